@@ -1,0 +1,351 @@
+#!/usr/bin/env python
+"""Benchmark: scheduling decisions/sec of the EdgeServing stability-score
+engine (BASELINE.json metric) on BASELINE configs[1] (default workload cfg2:
+4,096 scenarios x 4 DNNs x 4 exits x batch 1-16, 10k-request Poisson traces,
+rho_full 0.60-1.20, tau = 50 ms).
+
+One step = one pass of the whole hot path over the batch: K2 replay (a2-a8),
+K3 per-scenario P95 (a9) and the per-group merge (a10; NCCL all_reduce across
+ranks).  Inputs (164 MB of arrivals per rank) are resident in HBM and larger
+than the 126 MB L2, so no extra flush is needed.  Multi-GPU: each rank replays
+its own 4,096-scenario batch (weak scaling); only the group merge communicates.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+    torchrun --nproc-per-node N bench.py --gpus N ...
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "scheduling decisions/sec (stability-score evals)"
+UNIT = "decisions/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="cfg2")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--ncu", action="store_true", help="short run for ncu launch lists (no extras)")
+    return ap.parse_args()
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def rank_workload(name, rank):
+    """Weak scaling: rank r replays scenarios [r*S, (r+1)*S) of the config's
+    scenario sequence (same generator, same shapes, distinct seeds)."""
+    import inputs
+    S = inputs.total_scenarios(name)
+    ids = np.arange(rank * S, (rank + 1) * S, dtype=np.int64)
+    return inputs.workload(name, scen_ids=ids), S
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, bus_id):
+        self.bus_id = bus_id
+        self.rows = []
+        self.proc = None
+        self.th = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", self.bus_id, f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "50"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+            return
+        self.th = threading.Thread(target=self._read, daemon=True)
+        self.th.start()
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def stop(self):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+            self.th.join(timeout=5)
+        sm = []
+        reasons = set()
+        smax = None
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in self.rows:
+            try:
+                sm.append(float(r[0]))
+                smax = float(r[1])
+                for i, n in enumerate(names):
+                    if r[4 + i].lower().startswith("active"):
+                        reasons.add(n)
+            except (ValueError, IndexError):
+                continue
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": smax, "samples": len(sm),
+                "reasons": sorted(reasons)}
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return d.get("hbm_gbs", 6451.5), d.get("sm_max_mhz", 1965.0), "measured"
+    return 6650.0, 1965.0, "fallback"
+
+
+def ncu_traffic(kernel):
+    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(p):
+        return json.load(open(p)).get(kernel)
+    return None
+
+
+def alg_ops(stats_sum, requests, E):
+    """Algorithmic integer operations of Algorithm 1 per the op model of
+    DESIGN.md §6: 3 per Eq. 4 term (predicted-wait add, clip compare,
+    accumulate), 7 per live task (w = t - a, urgency table lookup and
+    product), 2 per examined (m, e) cell (Eq. 6 add + compare), 7 per
+    candidate (Eq. 5 + score finalisation + Eq. 7 compare), 4 per request
+    (admission compare, Eq. 1 latency, Eq. 2 compare, count), 2 per decision."""
+    d, c, cells, live, terms = (stats_sum[k] for k in ("decisions", "candidates", "cells", "live", "terms"))
+    return 3 * terms + 7 * live + 2 * cells + 7 * c + 4 * requests + 2 * d
+
+
+def run_reference(args, rank, world):
+    """--impl reference: the oracle (plain C, CPU) as it stands on the host cores."""
+    if rank != 0:
+        return
+    import oracle
+    w, S = rank_workload(args.workload, 0)
+    tr = w.traces
+    cores = os.cpu_count() or 1
+    chunk = 512
+    import inputs
+    nsteps = args.warmup + args.steps
+    times = []
+    dec = 0
+    for k in range(nsteps):
+        lo = (k * chunk) % S
+        ids = np.arange(lo, lo + chunk)
+        sub = inputs.workload(args.workload, scen_ids=ids)
+        t0 = time.perf_counter()
+        o = oracle.replay_batch(w.profile, w.cfgs, sub.traces, full=False, nthreads=cores)
+        dt = time.perf_counter() - t0
+        if k >= args.warmup:
+            times.append(dt)
+            dec += int(o["stats"][:, 0].sum())
+    tot = sum(times)
+    v = dec / tot
+    sample = f"{chunk} scenarios of {args.workload} per step (cycling through the {S}-scenario batch), full 10k-request traces"
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": 1e3 * tot / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "u32", "data": "synthetic",
+            "config": {"workload": f"{args.workload} (BASELINE configs[1])", "scenarios_per_step": chunk},
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": sample},
+            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse()
+    rank, world, local = dist_env()
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+    import torch
+    import torch.distributed as dist
+
+    import paper_2605_05527_b200 as es
+    from paper_2605_05527_b200 import engine
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    pg = None
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+        pg = dist.group.WORLD
+    import inputs
+
+    w, S = rank_workload(args.workload, rank)
+    G = inputs.n_groups(args.workload)
+    h = es.es_load_profile(w.profile, w.cfgs, device=local)
+    dtr = engine.upload_traces(w.traces, dev)
+    total = int(w.traces.arrival.size)
+    out = es.alloc_replay_out(h, S, total, dev, full=False, p95=True)
+    stream = torch.cuda.current_stream()
+    ev_k2 = []
+
+    def step(record):
+        if record:
+            a = torch.cuda.Event(enable_timing=True)
+            b = torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+        es.es_replay_traces(h, dtr["arr_off"], dtr["arrival"], dtr["cfg_idx"], dtr["group_id"], out=out,
+                            full=False, p95=False, stream=stream)
+        if record:
+            b.record(stream)
+            ev_k2.append((a, b))
+        es.es_scen_p95(h, dtr["arr_off"], dtr["arrival"], out, dtr["cfg_idx"], stream=stream)
+        return engine.group_merge(h, dtr, out, G, group=pg if world > 1 else False, stream=stream)
+
+    for _ in range(max(args.warmup, 1)):
+        counts, p95g = step(False)
+    torch.cuda.synchronize()
+    st = out["stats"].cpu().numpy()
+    assert int(st[:, 7].max()) == 0, "a scenario reported an error status"
+    cols = es.STAT_COLS
+    ssum = {c: int(st[:, i].sum()) for i, c in enumerate(cols)}
+    decisions_rank = ssum["decisions"]
+    cand_rank = ssum["candidates"]
+
+    # ---------------- timed region (device events, max over ranks)
+    bus = None
+    try:
+        p = torch.cuda.get_device_properties(dev)
+        bus = f"{p.pci_domain_id:08X}:{p.pci_bus_id:02X}:{p.pci_device_id:02X}.0"
+    except Exception:
+        pass
+    sampler = ClockSampler(bus) if (bus and not args.ncu) else None
+    if sampler:
+        sampler.start()
+        time.sleep(0.3)
+    l0 = h.launches
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    t0 = torch.cuda.Event(enable_timing=True)
+    t1 = torch.cuda.Event(enable_timing=True)
+    t0.record(stream)
+    for _ in range(args.steps):
+        step(True)
+    t1.record(stream)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clocks = sampler.stop() if sampler else None
+    launches = h.launches - l0 + 3 * args.steps  # + the three group-select kernels per step
+    ms = t0.elapsed_time(t1)
+    k2_ms = [a.elapsed_time(b) for a, b in ev_k2]
+    tt = torch.tensor([ms, float(decisions_rank), float(cand_rank)], dtype=torch.float64, device=dev)
+    if world > 1:
+        mx = tt[:1].clone()
+        dist.all_reduce(mx, op=dist.ReduceOp.MAX)
+        sm = tt[1:].clone()
+        dist.all_reduce(sm, op=dist.ReduceOp.SUM)
+        ms_max, dec_all, cand_all = float(mx[0]), float(sm[0]), float(sm[1])
+    else:
+        ms_max, dec_all, cand_all = ms, float(decisions_rank), float(cand_rank)
+    value = dec_all * args.steps / (ms_max / 1e3)
+
+    # ---------------- roofline of the dominant kernel (K2) -- issue/ALU bound
+    hbm, sm_max, src = peaks()
+    k2_avg_s = statistics.mean(k2_ms) / 1e3
+    ops = alg_ops(ssum, total, w.profile.E)
+    peak_ops = 148 * 128 * sm_max * 1e6  # INT32 lanes x clock (B300_MICROARCH alu+fma pipes)
+    achieved = ops / k2_avg_s
+    alg_bytes = 4 * total + 4 * total + 8 * 11 * S + 8 * (S * w.profile.M + 1)
+    roof = {"bound": "alu", "achieved": achieved / 1e9, "peak": peak_ops / 1e9, "unit": "Gop/s",
+            "frac": achieved / peak_ops, "traffic": ncu_traffic("k2_replay"), "kernel": "k2_replay",
+            "k2_ms": statistics.mean(k2_ms), "k2_share_of_step": statistics.mean(k2_ms) / (ms / args.steps),
+            "peak_source": f"148 SM x 128 INT32 lanes x {sm_max:.0f} MHz ({src} sm_max)",
+            "alg_ops_per_launch": ops,
+            "hbm_view": {"alg_bytes_per_launch": alg_bytes, "achieved_gbs": alg_bytes / k2_avg_s / 1e9,
+                         "peak_gbs": hbm, "frac": alg_bytes / k2_avg_s / 1e9 / hbm}}
+
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "u32", "data": "synthetic",
+            "config": {"workload": f"{args.workload} (BASELINE configs[1]): 4,096 scenarios/GPU x 4 DNNs x 4 exits "
+                                   f"x batch 1-16, 10k-request Poisson traces, rho 0.60-1.20, tau 50 ms",
+                       "scenarios_per_gpu": S, "requests_per_gpu": total, "groups": G,
+                       "l2": "inputs larger than L2 (164 MB arrivals/GPU > 126 MB)",
+                       "parallelism": f"scenario-sharded x{world}, NCCL all_reduce of group histograms"},
+            "scored_candidates_per_s": cand_all * args.steps / (ms_max / 1e3),
+            "decisions_per_step": dec_all, "gpu_launches": launches, "roofline": roof}
+    if clocks:
+        line["clocks"] = clocks
+
+    # ---------------- e2e through the host-buffer C-ABI call (rank-local)
+    if not args.no_e2e and not args.ncu:
+        pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory()
+        tr = w.traces
+        hin = [pin(tr.arr_off), pin(tr.arrival), pin(tr.cfg_idx), pin(tr.group_id)]
+        ho = {"stats": pin(np.zeros((S, es.ES_NSTAT), np.uint64)), "p95": pin(np.zeros(S, np.uint32)),
+              "dec_cap": 0}
+        for _ in range(2):
+            es.es_replay_traces_host(h, *hin, out=ho, stream=stream)
+        if world > 1:
+            dist.barrier()
+        n_e2e = max(3, min(args.steps, 20))
+        a = time.perf_counter()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(n_e2e):
+            es.es_replay_traces_host(h, *hin, out=ho, stream=stream)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        e_ms = e0.elapsed_time(e1)
+        wall_ms = (time.perf_counter() - a) * 1e3
+        et = torch.tensor([max(e_ms, wall_ms)], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(et, op=dist.ReduceOp.MAX)
+        e2e_v = dec_all * n_e2e / (float(et[0]) / 1e3)
+        h2d = sum(int(x.numel() * x.element_size()) for x in hin)
+        d2h = int(ho["stats"].numel() * 8 + ho["p95"].numel() * 4)
+        assert np.array_equal(ho["stats"].numpy(), st)
+        line["e2e"] = {"value": e2e_v, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+                       "steps": n_e2e, "call": "es_replay_traces_host (pinned host in/out, K2+K3)"}
+
+    # ---------------- CPU baseline: the oracle on the host cores (rank 0, N=1)
+    if rank == 0 and world == 1 and not args.no_cpu_baseline and not args.ncu:
+        import oracle
+        cores = os.cpu_count() or 1
+        t = time.perf_counter()
+        o = oracle.replay_batch(w.profile, w.cfgs, w.traces, full=False, nthreads=cores)
+        dt = time.perf_counter() - t
+        assert np.array_equal(o["stats"], st), "oracle and GPU disagree on the bench batch"
+        assert np.array_equal(o["p95"], out["p95"].cpu().numpy())
+        line["cpu_baseline"] = {"value": int(o["stats"][:, 0].sum()) / dt, "unit": UNIT, "cores": cores,
+                                "kind": "oracle",
+                                "sample": f"the full {S}-scenario bench batch (rank 0), one replay, "
+                                          f"{dt:.1f} s wall on {cores} threads",
+                                "parity": "bit-exact on all per-scenario counters and P95 of the batch"}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -37,9 +37,9 @@ _lock = threading.Lock()
 _lib = None
 
 F = 28  # fractional bits of the fixed-point score (reading Q5)
-NCOL = 9
+NCOL = 11
 COLS = ["decisions", "candidates", "cells", "completed", "violations", "infeasible",
-        "max_depth", "status", "sum_lat"]
+        "max_depth", "status", "sum_lat", "live", "terms"]
 
 
 def build(force=False):

@@ -350,7 +350,7 @@ int or_decide_batch(int M, int E, int nb, const int32_t *bs, const uint32_t *lat
 /* per-scenario statistics columns (same meaning as the library's, own enum) */
 enum {
   ST_DECISIONS = 0, ST_CANDIDATES, ST_CELLS, ST_COMPLETED, ST_VIOLATIONS,
-  ST_INFEASIBLE, ST_MAX_DEPTH, ST_STATUS, ST_SUM_LAT, ST_NCOL
+  ST_INFEASIBLE, ST_MAX_DEPTH, ST_STATUS, ST_SUM_LAT, ST_LIVE, ST_TERMS, ST_NCOL
 };
 
 static int cmp_u32(const void *a, const void *b) {
@@ -436,6 +436,13 @@ static int replay_one(const or_ctx *c, const uint64_t *n, const uint32_t *const 
     }
     stats[ST_DECISIONS]++;
     stats[ST_CANDIDATES] += (uint64_t)nc;
+    /* work counters: pending tasks not yet clipped at zero prediction (w < x_c)
+       and the Eq. 4 terms they generate (one per candidate) */
+    uint64_t live = 0;
+    for (int m = 0; m < M; ++m)
+      for (uint64_t i = 0; i < len[m]; ++i) live += (uint64_t)wbuf[m][i] < c->x_c;
+    stats[ST_LIVE] += live;
+    stats[ST_TERMS] += live * (uint64_t)nc;
     for (int m = 0; m < M; ++m)
       if (len[m]) stats[ST_CELLS] += (uint64_t)n_allowed(c, m);
     if (!d->feasible) stats[ST_INFEASIBLE]++;

@@ -1,0 +1,71 @@
+"""Host orchestration of the replay path and the per-group merge (step a10).
+
+Everything numeric runs in libedgeserve.so; this module only moves tensors,
+and (multi-GPU) calls torch.distributed.all_reduce(SUM) on the integer
+counters and histograms between the three radix-selection levels of the group
+P95.  Integer sums are order-independent, so the merged results are
+bit-identical for any number of ranks.
+"""
+from __future__ import annotations
+
+import numpy as np
+
+
+def upload_traces(traces, device, pin=False):
+    """inputs.Traces -> dict of CUDA tensors (u64 arr_off, u32 arrival, u16
+    cfg_idx, u32 group_id)."""
+    import torch
+
+    def t(a, dt):
+        x = torch.from_numpy(np.ascontiguousarray(a).view(dt_np[dt])).view(dt)
+        if pin:
+            x = x.pin_memory()
+        return x.to(device, non_blocking=pin)
+
+    dt_np = {torch.uint64: np.uint64, torch.uint32: np.uint32, torch.uint16: np.uint16}
+    return {"arr_off": t(traces.arr_off, torch.uint64), "arrival": t(traces.arrival, torch.uint32),
+            "cfg_idx": t(traces.cfg_idx, torch.uint16), "group_id": t(traces.group_id, torch.uint32)}
+
+
+def _all_reduce(x, group):
+    import torch
+    import torch.distributed as dist
+    if group is False or not dist.is_available() or not dist.is_initialized():
+        return
+    dist.all_reduce(x.view(torch.int64), op=dist.ReduceOp.SUM, group=group)
+
+
+def group_merge(prof, dtr, out, n_groups, group=None, stream=None):
+    """Exact per-group counters and nearest-rank P95 across all ranks.
+
+    dtr: uploaded traces of this rank's scenarios; out: this rank's replay
+    outputs.  group: a torch.distributed process group (None = default when
+    initialised, False = local only).  Returns (counts u64 [G][7], p95 u64 [G]).
+    """
+    import torch
+    from . import ES_HIST_BINS, ES_NGSTAT, es_group_accumulate, es_group_hist, es_group_p95_select
+    dev = dtr["arrival"].device
+    G = int(n_groups)
+    buf = torch.zeros(G * ES_NGSTAT + G * ES_HIST_BINS, dtype=torch.uint64, device=dev)
+    counts = buf[:G * ES_NGSTAT]
+    hist = buf[G * ES_NGSTAT:]
+    state = torch.zeros(2 * G, dtype=torch.uint64, device=dev)
+    es_group_accumulate(prof, dtr["arr_off"], dtr["arrival"], out, G, counts, hist, dtr["cfg_idx"],
+                        dtr["group_id"], stream)
+    _all_reduce(buf, group)
+    es_group_p95_select(G, 0, counts, hist, state, stream)
+    for level in (1, 2):
+        es_group_hist(prof, dtr["arr_off"], dtr["arrival"], out, G, level, state, hist, dtr["cfg_idx"],
+                      dtr["group_id"], stream)
+        _all_reduce(hist, group)
+        es_group_p95_select(G, level, counts, hist, state, stream)
+    return counts.view(G, ES_NGSTAT), state.view(G, 2)[:, 0]
+
+
+def replay_group_stats(prof, dtr, n_groups, full=False, group=None, stream=None, out=None):
+    """One pass of the whole hot path: K2 replay + K3 P95 + group merge."""
+    from . import es_replay_traces
+    out = es_replay_traces(prof, dtr["arr_off"], dtr["arrival"], dtr["cfg_idx"], dtr["group_id"], out=out,
+                           full=full, stream=stream)
+    counts, p95 = group_merge(prof, dtr, out, n_groups, group=group, stream=stream)
+    return out, counts, p95

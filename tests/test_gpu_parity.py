@@ -1,0 +1,281 @@
+"""GPU parity: the CUDA path (through the C ABI) against the oracle, bit-exact.
+
+Every comparison is element by element on the same seeded inputs (inputs/):
+tables, per-snapshot decisions and candidate scores (K1), per-request
+completion / exit / latency, decision logs and per-scenario counters (K2),
+per-scenario P95 (K3) and merged group statistics (a10).
+"""
+import numpy as np
+import pytest
+
+import inputs
+import oracle
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+import paper_2605_05527_b200 as es  # noqa: E402
+
+DEV = "cuda:0"
+
+
+def np_of(t):
+    return t.cpu().numpy() if t is not None else None
+
+
+def to_dev(a, dt):
+    m = {torch.uint64: np.uint64, torch.uint32: np.uint32, torch.uint16: np.uint16, torch.uint8: np.uint8}
+    return torch.from_numpy(np.ascontiguousarray(a).astype(m[dt])).to(DEV)
+
+
+# ------------------------------------------------------------------ tables
+
+@pytest.mark.parametrize("C", [1, 2, 10, 15])
+def test_tables_bitwise(C):
+    taus = [1024, 1500, 20000, 25000, 33333, 50000, 70001, 100000, 1 << 20]
+    prof = inputs.synth_profile(4, 4, list(range(1, 17)))
+    cfgs = [inputs.SchedCfg(tau=t, b_max=16, C=C) for t in taus]
+    # the image must fit shared memory: split the large-tau cfg out
+    for chunk in (cfgs[:-1], cfgs[-1:]):
+        h = es.es_load_profile(prof, chunk)
+        for k, c in enumerate(chunk):
+            g = es.es_get_tables(h, k)
+            o = oracle.build_tables(c.tau, C)
+            assert g["x_c"] == o["x_c"] and g["r"] == o["r"]
+            assert np.array_equal(g["A"], o["A"]), (c.tau, C)
+            assert np.array_equal(g["Bt"], o["Bt"])
+            for m in range(4):
+                for e in range(4):
+                    for b in range(16):
+                        L = int(prof.lat[m, e, b])
+                        exp = oracle.H(c.tau, L)[0] if L < o["x_c"] else np.iinfo(np.uint64).max
+                        assert int(g["H"][m, e, b]) == exp
+
+
+def test_profile_validation_errors():
+    p = inputs.synth_profile(3, 3, [1, 2, 4, 8])
+    bad = p.lat.copy()
+    bad[2, 1, 3] = bad[2, 0, 3]
+    with pytest.raises(es.EsError, match="MONOTONE.*m=2,e=1,b=3"):
+        es.es_load_profile(inputs.Profile(3, 3, p.bs, bad, p.mask), [inputs.SchedCfg(50000, 8)])
+    with pytest.raises(es.EsError, match="OUT_OF_GRID"):
+        es.es_load_profile(p, [inputs.SchedCfg(50000, 9)])
+    with pytest.raises(es.EsError, match="ARG"):
+        es.es_load_profile(p, [inputs.SchedCfg(500, 8)])
+    with pytest.raises(es.EsError, match="GRID"):
+        es.es_load_profile(inputs.Profile(3, 3, np.array([2, 4, 6, 8], np.int32), p.lat, p.mask),
+                           [inputs.SchedCfg(50000, 8)])
+
+
+# ------------------------------------------------------------------ K1
+
+def run_k1(prof, cfgs, q_off, waits, cfg_idx=None):
+    h = es.es_load_profile(prof, cfgs)
+    o = es.es_score_candidates(h, to_dev(q_off, torch.uint64), to_dev(waits, torch.uint32),
+                               None if cfg_idx is None else to_dev(cfg_idx, torch.uint16))
+    torch.cuda.synchronize()
+    return {k: np_of(v) for k, v in o.items()}
+
+
+def assert_k1_equal(g, o, M):
+    for k in ["m", "e", "B", "L", "S", "flags"]:
+        assert np.array_equal(g[k], o[k]), (k, np.nonzero(g[k] != o[k])[0][:10])
+    assert np.array_equal(g["cand"].reshape(-1, M), o["cand"])
+
+
+@pytest.mark.parametrize("M", [1, 2, 3, 4, 5, 8])
+def test_k1_random_states(M):
+    """SPEC-style random states: queues <= 10, waits in [0, 3 tau]."""
+    prof = inputs.synth_profile(M, 4, list(range(1, 11)), L_top=28000.0)
+    cfgs = [inputs.SchedCfg(tau=50000, b_max=10), inputs.SchedCfg(tau=20000, b_max=7)]
+    n = 3000
+    q_off, w = inputs.snapshots_uniform(40 + M, n, M, 10, 150000)
+    ci = (np.arange(n) % 2).astype(np.uint16)
+    assert_k1_equal(run_k1(prof, cfgs, q_off, w, ci), oracle.decide_batch(prof, cfgs, q_off, w, ci), M)
+
+
+@pytest.mark.parametrize("M,depth", [(4, 300), (8, 4096)])
+def test_k1_deep_snapshots(M, depth):
+    """5-C-style deep queues: long clipped prefixes counted, not read."""
+    prof = inputs.synth_profile(M, 5, list(range(1, 33)))
+    cfgs = [inputs.SchedCfg(tau=50000, b_max=32)]
+    rate = inputs.rates_for_shallow_load(prof, 32, 1.5)
+    q_off, w = inputs.snapshots_poisson_depth(7, np.arange(160), M, depth, rate)
+    assert_k1_equal(run_k1(prof, cfgs, q_off, w), oracle.decide_batch(prof, cfgs, q_off, w), M)
+
+
+def test_k1_masks_and_flags():
+    """exit masks (ablation), no-work, bad input, bad cfg index."""
+    prof = inputs.synth_profile(3, 4, [1, 2, 4, 8])
+    prof.mask = np.array([[1, 0, 0, 1], [0, 1, 1, 0], [0, 0, 0, 1]], np.uint8)
+    cfgs = [inputs.SchedCfg(tau=30000, b_max=8)]
+    q_off, w = inputs.snapshots_uniform(5, 800, 3, 9, 80000)
+    assert_k1_equal(run_k1(prof, cfgs, q_off, w), oracle.decide_batch(prof, cfgs, q_off, w), 3)
+    # no work + an inversion in the live window + a cfg index out of range
+    q = np.array([0, 0, 0, 0, 2, 3, 3, 4, 5, 6], np.uint64)
+    ws = np.array([10, 20, 7, 9, 8, 7], np.uint32)
+    g = run_k1(prof, cfgs, q, ws, np.array([0, 0, 5], np.uint16))
+    assert list(g["flags"]) == [2, 4, 4]
+
+
+def test_k1_harvested_snapshots():
+    """Snapshots harvested from oracle replays of cfg2/cfg3 traces."""
+    for name, ids in [("cfg2", [1, 7]), ("cfg3", [2, 11])]:
+        w = inputs.workload(name, scen_ids=ids, n_req=1500)
+        M = w.profile.M
+        cap = 3000
+        o = oracle.replay_batch(w.profile, w.cfgs, w.traces, dec_cap=cap)
+        q_off = [0]
+        ws = []
+        ci = []
+        for s in range(len(ids)):
+            arr = w.traces.scenario(s)
+            head = [0] * M
+            for k in range(int(o["stats"][s, 0])):
+                t = int(o["dec_t"][s * cap + k])
+                for m in range(M):
+                    tail = int(np.searchsorted(arr[m], t, side="right"))
+                    ws.extend(t - int(a) for a in arr[m][head[m]:tail])
+                    q_off.append(len(ws))
+                ci.append(int(w.traces.cfg_idx[s]))
+                head[int(o["dec_m"][s * cap + k])] += int(o["dec_B"][s * cap + k])
+        q_off = np.array(q_off, np.uint64)
+        ws = np.array(ws, np.uint32)
+        ci = np.array(ci, np.uint16)
+        g = run_k1(w.profile, w.cfgs, q_off, ws, ci)
+        r = oracle.decide_batch(w.profile, w.cfgs, q_off, ws, ci)
+        assert_k1_equal(g, r, M)
+
+
+# ------------------------------------------------------------------ K2 / K3
+
+def run_k2(w, full=True, dec_cap=0):
+    h = es.es_load_profile(w.profile, w.cfgs)
+    d = es.upload_traces(w.traces, DEV)
+    out = es.es_replay_traces(h, d["arr_off"], d["arrival"], d["cfg_idx"], d["group_id"], full=full,
+                              dec_cap=dec_cap)
+    torch.cuda.synchronize()
+    code, item = es.es_device_status(h)
+    res = {k: (np_of(v) if hasattr(v, "cpu") else v) for k, v in out.items()}
+    res["_handle"], res["_dev"], res["_out"] = h, d, out
+    res["_code"] = code
+    return res
+
+
+def assert_k2_equal(g, o, dec_cap=0):
+    assert np.array_equal(g["stats"], o["stats"]), np.nonzero((g["stats"] != o["stats"]).any(1))[0][:10]
+    assert np.array_equal(g["p95"], o["p95"])
+    if "completion" in o and g.get("completion") is not None:
+        assert np.array_equal(g["completion"], o["completion"])
+        assert np.array_equal(g["exit"], o["exit"])
+        assert np.array_equal(g["latency"], o["lat"])
+    if dec_cap:
+        for k in ["dec_t", "dec_m", "dec_e", "dec_B", "dec_L", "dec_S", "dec_f"]:
+            assert np.array_equal(g[k], o[k]), k
+
+
+@pytest.mark.parametrize("name,ids,n_req", [
+    ("cfg1", [0], None),
+    ("cfg2", list(range(0, 130, 3)), 2500),
+    ("cfg3", list(range(0, 117, 5)), 2000),
+])
+def test_k2_parity_configs(name, ids, n_req):
+    w = inputs.workload(name, scen_ids=ids, n_req=n_req)
+    cap = 4000
+    g = run_k2(w, dec_cap=cap)
+    o = oracle.replay_batch(w.profile, w.cfgs, w.traces, dec_cap=cap, nthreads=8)
+    assert g["_code"] == 0
+    assert_k2_equal(g, o, cap)
+
+
+def test_k2_deep_overload():
+    """5-B-shaped overload (rho_shallow 1.5): deep queues, clipped prefixes."""
+    w = inputs.workload("cfg5b", scen_ids=[0, 1, 2], n_req=12000)
+    g = run_k2(w)
+    o = oracle.replay_batch(w.profile, w.cfgs, w.traces, nthreads=3)
+    assert int(o["stats"][:, 6].max()) > 500  # really deep
+    assert_k2_equal(g, o)
+
+
+def test_k2_edge_cases():
+    prof = inputs.synth_profile(3, 3, [1, 2, 4, 8])
+    cfgs = [inputs.SchedCfg(tau=50000, b_max=8, warmup=0), inputs.SchedCfg(tau=20000, b_max=3, warmup=2)]
+    scen = [
+        [[], [], []],                      # empty scenario
+        [[0], [], []],                     # single request
+        [[5] * 40, [5] * 3, [5]],          # everything at one instant (Q10)
+        [[], [], list(range(0, 100000, 7))],  # one busy model only
+        [[10, 10, 4000000000], [], []],    # long idle gap (Q12)
+        [[1, 2, 3], [7, 8], []],
+    ]
+    segs = [[np.asarray(q, np.uint32) for q in sc] for sc in scen]
+    n = len(scen)
+    tr = inputs._assemble(3, segs, [i % 2 for i in range(n)], [0] * n, np.arange(n))
+    w = inputs.Workload("edge", prof, cfgs, tr, 0)
+    g = run_k2(w, dec_cap=64)
+    o = oracle.replay_batch(prof, cfgs, tr, dec_cap=64)
+    assert_k2_equal(g, o, 64)
+
+
+def test_k2_errors():
+    prof = inputs.synth_profile(2, 2, [1, 2])
+    cfgs = [inputs.SchedCfg(tau=50000, b_max=2, warmup=0)]
+    scen = [[[5, 3], []], [[0xFFFFFFF0], [1]], [[1], [2]]]  # unsorted, u32 overflow, fine
+    segs = [[np.asarray(q, np.uint32) for q in sc] for sc in scen]
+    tr = inputs._assemble(2, segs, [0, 0, 0], [0] * 3, np.arange(3))
+    w = inputs.Workload("err", prof, cfgs, tr, 0)
+    g = run_k2(w)
+    o = oracle.replay_batch(prof, cfgs, tr)
+    assert int(g["stats"][0, 7]) == 8 and int(o["stats"][0, 7]) != 0  # ES_ERR_UNSORTED
+    assert int(g["stats"][1, 7]) == 5 and int(o["stats"][1, 7]) == 3  # ES_ERR_RANGE / oracle RANGE
+    assert np.array_equal(g["stats"][2], o["stats"][2])
+    assert g["_code"] in (5, 8)
+
+
+def test_group_merge_matches_oracle():
+    w = inputs.workload("cfg2", scen_ids=np.arange(52), n_req=1500)
+    g = run_k2(w)
+    counts, p95 = es.group_merge(g["_handle"], g["_dev"], g["_out"], 13, group=False)
+    torch.cuda.synchronize()
+    o = oracle.replay_batch(w.profile, w.cfgs, w.traces, nthreads=8)
+    oc, op = oracle.group_stats(w.traces, o, w.cfgs, 13)
+    assert np.array_equal(np_of(counts), oc)
+    assert np.array_equal(np_of(p95).astype(np.uint32), op)
+
+
+def test_host_entry_point_matches_device():
+    w = inputs.workload("cfg2", scen_ids=np.arange(20), n_req=1200)
+    h = es.es_load_profile(w.profile, w.cfgs)
+    tr = w.traces
+    total = tr.arrival.size
+    pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory()
+    ho = {"latency": pin(np.zeros(total, np.uint32)), "stats": pin(np.zeros((tr.n_scen, es.ES_NSTAT), np.uint64)),
+          "p95": pin(np.zeros(tr.n_scen, np.uint32)), "completion": pin(np.zeros(total, np.uint32)),
+          "exit": pin(np.zeros(total, np.uint8)), "dec_cap": 0}
+    es.es_replay_traces_host(h, pin(tr.arr_off), pin(tr.arrival), pin(tr.cfg_idx), pin(tr.group_id), out=ho)
+    o = oracle.replay_batch(w.profile, w.cfgs, tr, nthreads=4)
+    g = {k: (v.numpy() if hasattr(v, "numpy") else v) for k, v in ho.items()}
+    assert_k2_equal(g, o)
+
+
+def test_full_size_cfg2_bench_config():
+    """BASELINE configs[1] at full size in the bench's launch configuration:
+    every scenario's counters and P95 against the oracle (16 host threads),
+    plus full per-request outputs on a sample of scenarios."""
+    w = inputs.workload("cfg2")
+    g = run_k2(w, full=False)
+    o = oracle.replay_batch(w.profile, w.cfgs, w.traces, full=True, nthreads=16)
+    assert np.array_equal(g["stats"], o["stats"])
+    assert np.array_equal(g["p95"], o["p95"])
+    assert np.array_equal(g["latency"], o["lat"])
+    counts, p95 = es.group_merge(g["_handle"], g["_dev"], g["_out"], 13, group=False)
+    oc, op = oracle.group_stats(w.traces, o, w.cfgs, 13)
+    assert np.array_equal(np_of(counts), oc) and np.array_equal(np_of(p95).astype(np.uint32), op)
+
+
+def test_determinism_repeat():
+    w = inputs.workload("cfg3", scen_ids=np.arange(40), n_req=800)
+    a = run_k2(w)
+    b = run_k2(w)
+    for k in ["stats", "p95", "completion", "exit", "latency"]:
+        assert np.array_equal(a[k], b[k])
