@@ -83,10 +83,25 @@ def lib():
         L.es_version.restype = ctypes.c_char_p
         L.es_launch_count.restype = ctypes.c_int64
         L.es_launch_count.argtypes = [P]
-        for f in ["es_load_profile", "es_free_profile", "es_get_tables", "es_score_candidates",
-                  "es_replay_traces", "es_scen_p95", "es_replay_traces_host", "es_group_accumulate", "es_group_hist",
-                  "es_group_p95_select", "es_device_status"]:
-            getattr(L, f).restype = ctypes.c_int
+        i32, u32, i64 = ctypes.c_int32, ctypes.c_uint32, ctypes.c_int64
+        sig = {
+            "es_load_profile": [P, P, i32, i32, P],
+            "es_free_profile": [P],
+            "es_get_tables": [P, i32, P, P, P, P, i32, P, P],
+            "es_score_candidates": [P, P, P, P],
+            "es_replay_traces": [P, P, P, P],
+            "es_scen_p95": [P, P, P, P],
+            "es_replay_traces_host": [P, P, P, P],
+            "es_group_accumulate": [P, P, P, u32, P, P, P],
+            "es_group_hist": [P, P, P, u32, i32, P, P, P],
+            "es_group_p95_select": [u32, i32, P, P, P, P],
+            "es_device_status": [P, P, P, P],
+        }
+        for f, args in sig.items():
+            fn = getattr(L, f)
+            fn.restype = ctypes.c_int
+            fn.argtypes = args
+        del i64
         _lib = L
     return _lib
 

@@ -179,11 +179,15 @@ __global__ void __launch_bounds__(NT) k_group_level(GroupArgs a) {
     const uint32_t *src = a.lat + base + W;
     for (int i = threadIdx.x; i < BINS; i += NT) hist[i] = 0u;
     __syncthreads();
-    for (uint32_t i = threadIdx.x; i < n; i += NT) {
-      const uint32_t v = src[i];
+    for (uint32_t i0 = 0; i0 < n; i0 += NT) {  // whole warps iterate together (ballot below)
+      const uint32_t i = i0 + threadIdx.x;
+      const uint32_t v = i < n ? src[i] : 0u;
       uint32_t bin;
       bool take;
-      if (a.level == 0) {
+      if (i >= n) {
+        bin = 0u;
+        take = false;
+      } else if (a.level == 0) {
         bin = v >> 20;
         take = true;
       } else if (a.level == 1) {
