@@ -1,21 +1,22 @@
 // decide.cuh -- one scheduling decision (Algorithm 1) evaluated by
-// one warp, shared by K1 (snapshots) and K2 (trace replay).
+// a segment of LPS lanes of a warp, shared by K1 (snapshots) and K2 (replay).
 //
-// Warp layout: the 32 lanes form MM groups of GL = 32/MM lanes; group g owns
-// model g's queue Q_g.  Per decision:
+// Lane layout: a warp holds 32/LPS independent segments (one scenario or
+// snapshot each).  A segment's LPS lanes form MM groups of GL = LPS/MM lanes;
+// group g owns model g's queue Q_g.  Per decision:
 //   a3  Eq. 5: B*_g = largest profiled batch <= min(|Q_g|, B_max)
 //       (reading Q8; SMEM table bidx).
 //   a4  Eq. 6: the GL lanes of group g test one exit each against
 //       w_max + L(g, e, B*) <= tau; the deepest passing exit is the top bit of
 //       the group's ballot (reading Q2: none passes -> shallowest allowed,
 //       infeasible).
-//   a5  prediction: never materialised; a candidate m with latency
+//   a5  prediction: never materialised; candidate m with latency
 //       L_m clips a remaining task iff its predicted wait w + L_m >= x_c, i.e.
 //       w >= thr_m = x_c - L_m; candidate m's own B*_m head tasks are excluded
 //       (P:364).
-//   a6  Eq. 3-4 in fixed point (reading Q5): every lane walks its group's live
-//       window once, evaluates G(w) once per task (2 LDS + IMAD.WIDE + SHF) and
-//       accumulates (K_m, U_m) for all candidates m; tasks with w >= x_c (the
+//   a6  Eq. 3-4 in fixed point (reading Q5): each lane walks its group's live
+//       window, evaluates G(w) once per task (2 LDS + IMAD.WIDE + SHF) and
+//       accumulates (K_m, U_m) for every candidate m; tasks with w >= x_c (the
 //       clipped-for-everyone prefix) are counted from the index, never read.
 //       S_q(m) = C_q K_m + floor(H(L_m) U_m / 2^28).
 //   a7  Eq. 7: argmin of the key (S_q(m), m) -- lowest model index
@@ -32,15 +33,16 @@ namespace es {
 
 constexpr unsigned FULL = 0xffffffffu;
 
-struct SmemCfg {  // per-cfg pointers into the staged SMEM image
-  const uint32_t *A, *Bt;
-  const uint64_t *H;
-  const uint8_t *bidx;
+// per-cfg constants, held in registers by every lane of a segment
+struct SmemCfg {
+  uint32_t off_A, off_Bt, off_H, off_bidx;  // byte offsets into the staged image
   uint32_t tau, b_max, warmup, x_c, r, nA1;
+  uint32_t fast_lim;  // head waits below it cannot clip for any candidate
   uint64_t C_q;
 };
 
 struct SmemProf {
+  const uint8_t *sm;
   const uint32_t *lat;
   const uint16_t *bs;
   const uint32_t *mask;
@@ -50,6 +52,7 @@ struct SmemProf {
 
 __device__ __forceinline__ SmemProf smem_prof(const uint8_t *sm, const ImgLayout &lay) {
   SmemProf p;
+  p.sm = sm;
   p.lat = reinterpret_cast<const uint32_t *>(sm + lay.off_lat);
   p.bs = reinterpret_cast<const uint16_t *>(sm + lay.off_bs);
   p.mask = reinterpret_cast<const uint32_t *>(sm + lay.off_mask);
@@ -61,30 +64,32 @@ __device__ __forceinline__ SmemProf smem_prof(const uint8_t *sm, const ImgLayout
   return p;
 }
 
-__device__ __forceinline__ SmemCfg smem_cfg(const uint8_t *sm, const SmemProf &p, int k) {
+__device__ __forceinline__ SmemCfg smem_cfg(const SmemProf &p, int k) {
   const CfgRec &c = p.cfg[k];
   SmemCfg s;
-  s.A = reinterpret_cast<const uint32_t *>(sm + c.off_A);
-  s.Bt = reinterpret_cast<const uint32_t *>(sm + c.off_Bt);
-  s.H = reinterpret_cast<const uint64_t *>(sm + c.off_H);
-  s.bidx = sm + c.off_bidx;
+  s.off_A = c.off_A;
+  s.off_Bt = c.off_Bt;
+  s.off_H = c.off_H;
+  s.off_bidx = c.off_bidx;
   s.tau = c.tau;
   s.b_max = c.b_max;
   s.warmup = c.warmup;
   s.x_c = c.x_c;
   s.r = c.r;
   s.nA1 = c.nA - 1u;
+  s.fast_lim = c.fast_lim;
   s.C_q = c.C_q;
   return s;
 }
 
 // G(w) = (A[(w+r)>>10] * Bt[(w+r)&1023]) >> 28 for w < x_c (reading Q5).
 // w >= x_c is clamped (its value is never used: such a task clips for all).
-__device__ __forceinline__ uint32_t G_of(const SmemCfg &c, uint32_t w) {
-  uint32_t v = min(w, c.x_c) + c.r;
-  uint32_t h = min(v >> SBITS, c.nA1);
-  uint64_t prod = (uint64_t)c.A[h] * (uint64_t)c.Bt[v & (S - 1u)];
-  return (uint32_t)(prod >> F);
+__device__ __forceinline__ uint32_t G_of(const SmemProf &P, const SmemCfg &c, uint32_t w) {
+  const uint32_t v = min(w, c.x_c) + c.r;
+  const uint32_t h = min(v >> SBITS, c.nA1);
+  const uint32_t a = *reinterpret_cast<const uint32_t *>(P.sm + c.off_A + 4u * h);
+  const uint32_t b = *reinterpret_cast<const uint32_t *>(P.sm + c.off_Bt + 4u * (v & (S - 1u)));
+  return (uint32_t)(((uint64_t)a * (uint64_t)b) >> F);
 }
 
 // Stage the profile image into shared memory with TMA 1-D bulk copies that
@@ -121,75 +126,120 @@ __device__ __forceinline__ void stage_image(uint8_t *smem, const uint8_t *gimg, 
   }
 }
 
-template <int MM>
-struct Lanes {
-  static constexpr int GL = 32 / MM;
-  int lane, grp, gl;
-  unsigned gmask;  // this group's lanes
-  __device__ __forceinline__ Lanes() {
+__device__ __forceinline__ constexpr unsigned low_mask(int n) { return n >= 32 ? FULL : ((1u << n) - 1u); }
+
+// Lane roles inside a warp: 32/LPS segments, MM groups of GL lanes each.
+// Reductions use compile-time-constant masks (a runtime mask makes ptxas emit
+// a collective loop): REDUX over the full warp when LPS == 32, xor-shuffle
+// butterflies of width LPS / GL otherwise.
+template <int LPS, int MM>
+struct Seg {
+  static_assert(LPS == 8 || LPS == 16 || LPS == 32, "LPS");
+  static_assert(MM <= LPS && (LPS % MM) == 0, "MM");
+  static constexpr int GL = LPS / MM;
+  int lane, seg, sl, grp, gl, seg_base;
+  __device__ __forceinline__ Seg() {
     lane = threadIdx.x & 31;
-    grp = lane / GL;
-    gl = lane % GL;
-    gmask = (GL == 32) ? FULL : (((1u << GL) - 1u) << (grp * GL));
+    seg = lane / LPS;
+    sl = lane % LPS;
+    grp = sl / GL;
+    gl = sl % GL;
+    seg_base = seg * LPS;
   }
-  // group-local bits of a warp ballot, shifted to bit 0
+  // this group's bits of a warp ballot, shifted to bit 0
   __device__ __forceinline__ unsigned gbits(unsigned ballot) const {
-    return (GL == 32) ? ballot : ((ballot >> (grp * GL)) & ((1u << GL) - 1u));
+    return (ballot >> (seg_base + grp * GL)) & low_mask(GL);
+  }
+  // this segment's bits of a warp ballot
+  __device__ __forceinline__ unsigned sbits(unsigned ballot) const {
+    return LPS == 32 ? ballot : (ballot >> seg_base) & low_mask(LPS);
+  }
+  __device__ __forceinline__ bool seg_any(bool p) const { return sbits(__ballot_sync(FULL, p)) != 0u; }
+  __device__ __forceinline__ uint32_t sum(uint32_t v) const {
+    if constexpr (LPS == 32) {
+      return __reduce_add_sync(FULL, v);
+    } else {
+#pragma unroll
+      for (int o = LPS / 2; o >= 1; o >>= 1) v += __shfl_xor_sync(FULL, v, o, LPS);
+      return v;
+    }
+  }
+  __device__ __forceinline__ uint32_t vmin(uint32_t v) const {
+    if constexpr (LPS == 32) {
+      return __reduce_min_sync(FULL, v);
+    } else {
+#pragma unroll
+      for (int o = LPS / 2; o >= 1; o >>= 1) v = min(v, __shfl_xor_sync(FULL, v, o, LPS));
+      return v;
+    }
+  }
+  __device__ __forceinline__ uint32_t vmax(uint32_t v) const {
+    if constexpr (LPS == 32) {
+      return __reduce_max_sync(FULL, v);
+    } else {
+#pragma unroll
+      for (int o = LPS / 2; o >= 1; o >>= 1) v = max(v, __shfl_xor_sync(FULL, v, o, LPS));
+      return v;
+    }
+  }
+  // exact segment sum of u64 values < 2^51 each (24 | 27-bit halves for REDUX)
+  __device__ __forceinline__ uint64_t sum64(uint64_t v) const {
+    if constexpr (LPS == 32) {
+      const uint32_t lo = (uint32_t)(v & 0xFFFFFFu);
+      const uint32_t hi = (uint32_t)(v >> 24);
+      return ((uint64_t)__reduce_add_sync(FULL, hi) << 24) + (uint64_t)__reduce_add_sync(FULL, lo);
+    } else {
+#pragma unroll
+      for (int o = LPS / 2; o >= 1; o >>= 1) v += __shfl_xor_sync(FULL, v, o, LPS);
+      return v;
+    }
+  }
+  // exact group sum of u64 values
+  __device__ __forceinline__ uint64_t gsum64(uint64_t v) const {
+#pragma unroll
+    for (int o = GL / 2; o >= 1; o >>= 1) v += __shfl_xor_sync(FULL, v, o, GL);
+    return v;
+  }
+  template <typename T>
+  __device__ __forceinline__ T bcast(T v, int src_sl) const {
+    return __shfl_sync(FULL, v, src_sl, LPS);
   }
 };
 
-__device__ __forceinline__ uint32_t red_u32(uint32_t v) { return __reduce_add_sync(FULL, v); }
-// exact warp sum of u64 values < 2^51 each: split 24 | 27 bits into two u32 reductions
-__device__ __forceinline__ uint64_t red_u64(uint64_t v) {
-  uint32_t lo = (uint32_t)(v & 0xFFFFFFu);
-  uint32_t hi = (uint32_t)(v >> 24);
-  return ((uint64_t)__reduce_add_sync(FULL, hi) << 24) + (uint64_t)__reduce_add_sync(FULL, lo);
-}
-template <int GL>
-__device__ __forceinline__ uint32_t grp_sum_u32(uint32_t v) {
-#pragma unroll
-  for (int o = GL / 2; o >= 1; o >>= 1) v += __shfl_xor_sync(FULL, v, o, GL);
-  return v;
-}
-template <int GL>
-__device__ __forceinline__ uint64_t grp_sum_u64(uint64_t v) {
-#pragma unroll
-  for (int o = GL / 2; o >= 1; o >>= 1) v += __shfl_xor_sync(FULL, v, o, GL);
-  return v;
-}
-
 // per-group candidate (uniform across the group's lanes)
 struct Cand {
-  uint32_t B, bi, e, L, thr;
+  uint32_t B, e, L, thr;
   uint64_t H;
   bool feas;
 };
 
-// a3 + a4 for the group's own model g (valid when len > 0).  Must be called
-// by the whole warp (contains ballots).
-template <int MM>
-__device__ __forceinline__ Cand cand_params(const Lanes<MM> &ln, const SmemProf &P, const SmemCfg &C,
-                                            int g, uint32_t len, uint32_t wmax) {
-  constexpr int GL = Lanes<MM>::GL;
+// a3 + a4 for the group's own model g (valid when len > 0).  Whole warp.
+template <int LPS, int MM>
+__device__ __forceinline__ Cand cand_params(const Seg<LPS, MM> &sg, const SmemProf &P, const SmemCfg &C,
+                                            uint32_t len, uint32_t wmax) {
+  constexpr int GL = Seg<LPS, MM>::GL;
   Cand k;
   const uint32_t cap = len < C.b_max ? len : C.b_max;
-  const int gg = g < P.M ? g : 0;
-  k.bi = C.bidx[cap];
-  k.B = P.bs[k.bi];
+  const int gg = sg.grp < P.M ? sg.grp : 0;
+  const uint32_t bi = P.sm[C.off_bidx + cap];
+  k.B = P.bs[bi];
   const uint32_t mbits = P.mask[gg];
-  const uint32_t *row = P.lat + (size_t)gg * P.E * P.nb + k.bi;  // row[e * nb]
+  const uint32_t *row = P.lat + (size_t)gg * P.E * P.nb + bi;  // row[e * nb]
   unsigned bits = 0;
-  for (int e0 = 0; e0 < P.E; e0 += GL) {  // warp-uniform trip count
-    const int e = e0 + ln.gl;
+#pragma unroll
+  for (int e0 = 0; e0 < MAXE; e0 += GL) {  // compile-time trip count, E <= MAXE
+    if (e0 >= P.E) break;                 // warp-uniform
+    const int e = e0 + sg.gl;
     bool ok = false;
     if (e < P.E && ((mbits >> e) & 1u)) ok = (uint64_t)wmax + row[e * P.nb] <= (uint64_t)C.tau;
-    bits |= ln.gbits(__ballot_sync(FULL, ok)) << e0;
+    bits |= sg.gbits(__ballot_sync(FULL, ok)) << e0;
   }
   k.feas = bits != 0u;
   k.e = k.feas ? 31u - __clz(bits) : (uint32_t)(__ffs(mbits) - 1);
   k.L = row[k.e * P.nb];
   k.thr = k.L < C.x_c ? C.x_c - k.L : 0u;
-  k.H = k.L < C.x_c ? C.H[((size_t)gg * P.E + k.e) * P.nb + k.bi] : 0ull;
+  k.H = k.L < C.x_c ? reinterpret_cast<const uint64_t *>(P.sm + C.off_H)[((size_t)gg * P.E + k.e) * P.nb + bi]
+                    : 0ull;
   return k;
 }
 
@@ -200,76 +250,16 @@ struct Decision {
   bool feas;
 };
 
-// a5-a7.  Inputs per group g (uniform in the group): len = |Q_g|, c = number of
-// head tasks with w >= x_c (clipped for everyone, never read), cand = a3/a4
-// result, and wait_at(p) returning the wait of position p (c <= p < len).
-// Returns the decision (uniform across the warp).  Unused groups: len = 0.
-template <int MM, class WaitAt>
-__device__ __forceinline__ Decision decide(const Lanes<MM> &ln, const SmemCfg &C, uint32_t len, uint32_t c,
-                                           const Cand &cand, WaitAt wait_at) {
-  constexpr int GL = Lanes<MM>::GL;
-  // broadcast every candidate's clip threshold thr_m = x_c - L_m
-  uint32_t thr[MM];
-#pragma unroll
-  for (int m = 0; m < MM; ++m) thr[m] = __shfl_sync(FULL, cand.thr, m * GL);
-  uint32_t K[MM];
-  uint64_t U[MM];
-#pragma unroll
-  for (int m = 0; m < MM; ++m) {
-    K[m] = 0u;
-    U[m] = 0ull;
-  }
-  uint32_t Kx = 0u;  // own served tasks (positions < B*_g) -- excluded for candidate g
-  uint64_t Ux = 0ull;
-  const uint32_t Bown = len ? cand.B : 0u;
-  for (uint32_t p = c + ln.gl; p < len; p += GL) {
-    const uint32_t w = wait_at(p);
-    const uint32_t gw = G_of(C, w);
-#pragma unroll
-    for (int m = 0; m < MM; ++m) {
-      if (w >= thr[m]) K[m] += 1u;
-      else U[m] += gw;
-    }
-    if (p < Bown) {
-      if (w >= cand.thr) Kx += 1u;
-      else Ux += gw;
-    }
-  }
-  // exact reductions
-#pragma unroll
-  for (int m = 0; m < MM; ++m) {
-    K[m] = red_u32(K[m]);
-    U[m] = red_u64(U[m]);
-  }
-  Kx = grp_sum_u32<GL>(Kx);
-  Ux = grp_sum_u64<GL>(Ux);
-  const uint32_t cpre = red_u32(ln.gl == 0 ? c : 0u);
-  uint32_t k_own = 0u;
-  uint64_t u_own = 0ull;
-#pragma unroll
-  for (int m = 0; m < MM; ++m)
-    if (m == ln.grp) {
-      k_own = K[m];
-      u_own = U[m];
-    }
-  // Eq. 4 on the predicted state of candidate g (P:364: served tasks excluded)
-  const uint32_t cB = c < Bown ? c : Bown;
-  const uint64_t Ktot = (uint64_t)(k_own - Kx) + (uint64_t)(cpre - cB);
-  const uint64_t Utot = u_own - Ux;
-  uint64_t Sq = ~0ull;
-  uint32_t mkey = 0xFFu;
-  if (len) {
-    // floor(H * U / 2^28) via the 128-bit product
-    const uint64_t lo = cand.H * Utot, hi = __umul64hi(cand.H, Utot);
-    Sq = C.C_q * Ktot + ((hi << (64 - F)) | (lo >> F));
-    mkey = (uint32_t)ln.grp;
-  }
+// a7: Eq. 7 argmin of (S, m) across the segment's groups + winner broadcast
+template <int LPS, int MM>
+__device__ __forceinline__ Decision finish_decision(const Seg<LPS, MM> &sg, const Cand &cand, uint64_t Sq,
+                                                   uint32_t mkey) {
+  constexpr int GL = Seg<LPS, MM>::GL;
   const uint64_t S_own = Sq;
-  // Eq. 7: argmin of (S, m) across groups
 #pragma unroll
-  for (int o = GL; o < 32; o <<= 1) {
-    const uint64_t So = __shfl_xor_sync(FULL, Sq, o);
-    const uint32_t mo = __shfl_xor_sync(FULL, mkey, o);
+  for (int o = GL; o < LPS; o <<= 1) {
+    const uint64_t So = __shfl_xor_sync(FULL, Sq, o, LPS);
+    const uint32_t mo = __shfl_xor_sync(FULL, mkey, o, LPS);
     if (So < Sq || (So == Sq && mo < mkey)) {
       Sq = So;
       mkey = mo;
@@ -280,12 +270,114 @@ __device__ __forceinline__ Decision decide(const Lanes<MM> &ln, const SmemCfg &C
   d.S_own = S_own;
   d.m = mkey;
   const int src = (int)(mkey & (MM - 1)) * GL;
-  const uint32_t pk = __shfl_sync(FULL, cand.e | (cand.feas ? 0x80u : 0u) | (cand.B << 8), src);
-  d.L = __shfl_sync(FULL, cand.L, src);
+  const uint32_t pk = sg.bcast(cand.e | (cand.feas ? 0x80u : 0u) | (cand.B << 8), src);
+  d.L = sg.bcast(cand.L, src);
   d.e = pk & 0x7Fu;
   d.feas = (pk & 0x80u) != 0u;
   d.B = pk >> 8;
   return d;
+}
+
+template <int LPS, int MM, class WaitAt>
+__device__ __forceinline__ Decision decide_general(const Seg<LPS, MM> &sg, const SmemProf &P, const SmemCfg &C,
+                                                uint32_t len, uint32_t c, const Cand &cand, uint32_t Bown,
+                                                WaitAt wait_at) {
+  constexpr int GL = Seg<LPS, MM>::GL;
+  // every candidate's clip threshold thr_m = x_c - L_m
+  uint32_t thr[MM];
+#pragma unroll
+  for (int m = 0; m < MM; ++m) thr[m] = sg.bcast(cand.thr, m * GL);
+  uint32_t K[MM];
+  uint64_t U[MM];
+#pragma unroll
+  for (int m = 0; m < MM; ++m) {
+    K[m] = 0u;
+    U[m] = 0ull;
+  }
+  uint32_t p = c + sg.gl;
+  // own served head tasks (positions < B*_g): count for every candidate but g
+  for (; p < len && p < Bown; p += GL) {
+    const uint32_t w = wait_at(p);
+    const uint32_t gw = G_of(P, C, w);
+#pragma unroll
+    for (int m = 0; m < MM; ++m) {
+      if (m == sg.grp) continue;
+      if (w >= thr[m]) K[m] += 1u;
+      else U[m] += gw;
+    }
+  }
+  for (; p < len; p += GL) {
+    const uint32_t w = wait_at(p);
+    const uint32_t gw = G_of(P, C, w);
+#pragma unroll
+    for (int m = 0; m < MM; ++m) {
+      if (w >= thr[m]) K[m] += 1u;
+      else U[m] += gw;
+    }
+  }
+  // exact segment reductions; each group keeps its own candidate's sums
+  uint32_t k_own = 0u;
+  uint64_t u_own = 0ull;
+#pragma unroll
+  for (int m = 0; m < MM; ++m) {
+    if (m >= P.M) break;  // warp-uniform
+    const uint32_t k = sg.sum(K[m]);
+    const uint64_t u = sg.sum64(U[m]);
+    if (m == sg.grp) {
+      k_own = k;
+      u_own = u;
+    }
+  }
+  const uint32_t cpre = sg.sum(sg.gl == 0 ? c : 0u);
+  // Eq. 4 on the predicted state of candidate g (P:364: served tasks excluded)
+  const uint32_t cB = c < Bown ? c : Bown;
+  const uint64_t Ktot = (uint64_t)k_own + (uint64_t)(cpre - cB);
+  uint64_t Sq = ~0ull;
+  uint32_t mkey = 0xFFu;
+  if (len) {
+    // floor(H * U / 2^28) via the 128-bit product
+    const uint64_t lo = cand.H * u_own, hi = __umul64hi(cand.H, u_own);
+    Sq = C.C_q * Ktot + ((hi << (64 - F)) | (lo >> F));
+    mkey = (uint32_t)sg.grp;
+  }
+  return finish_decision<LPS, MM>(sg, cand, Sq, mkey);
+}
+
+// a5-a7.  Inputs per group g (uniform in the group): len = |Q_g|, c = number of
+// head tasks with w >= x_c (clipped for everyone, never read), cand = a3/a4
+// result, and wait_at(p) returning the wait of position p (c <= p < len; no
+// warp-synchronous operation inside).  Returns the segment's decision
+// (uniform across the segment).  Empty groups / inactive segments: len = 0.
+template <int LPS, int MM, class WaitAt>
+__device__ __forceinline__ Decision decide(const Seg<LPS, MM> &sg, const SmemProf &P, const SmemCfg &C,
+                                           uint32_t len, uint32_t c, uint32_t wmax, const Cand &cand,
+                                           WaitAt wait_at) {
+  constexpr int GL = Seg<LPS, MM>::GL;
+  const uint32_t Bown = len ? cand.B : 0u;
+  uint64_t Sq = ~0ull;
+  uint32_t mkey = 0xFFu;
+  // Fast path (same integers): when every head wait is below x_c - max L, no
+  // task of any queue can reach x_c under any candidate's prediction, so
+  // K_m = 0 and U_m = sum_all G - sum_{own served} G for every m.  The
+  // per-candidate clip tests and 3 M reductions collapse to 4 reductions.
+  if (!__any_sync(FULL, len > 0u && wmax >= C.fast_lim)) {
+    uint64_t tot = 0ull, srv = 0ull;
+    for (uint32_t p = sg.gl; p < len; p += GL) {
+      const uint64_t gw = G_of(P, C, wait_at(p));
+      tot += gw;
+      if (p < Bown) srv += gw;
+    }
+    tot = sg.sum64(tot);
+    srv = sg.gsum64(srv);
+    if (len) {
+      const uint64_t u = tot - srv;
+      const uint64_t lo = cand.H * u, hi = __umul64hi(cand.H, u);
+      Sq = (hi << (64 - F)) | (lo >> F);
+      mkey = (uint32_t)sg.grp;
+    }
+    return finish_decision<LPS, MM>(sg, cand, Sq, mkey);
+  }
+  return decide_general<LPS, MM>(sg, P, C, len, c, cand, Bown, wait_at);
 }
 
 }  // namespace es

@@ -27,8 +27,8 @@ struct __align__(16) CfgRec {
   uint32_t x_c, r, nA, nA_cap;
   uint64_t C_q;
   uint32_t off_A, off_Bt, off_H, off_bidx;
-  uint32_t status;  // ES_OK or ES_ERR_NUMERIC (set by k_build_tables)
-  uint32_t pad;
+  uint32_t status;    // ES_OK or ES_ERR_NUMERIC (set by k_build_tables)
+  uint32_t fast_lim;  // x_c - max L over the profile (0 if <= 0): waits below it never clip
 };
 static_assert(sizeof(CfgRec) == 64, "CfgRec layout");
 

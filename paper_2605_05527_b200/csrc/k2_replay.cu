@@ -1,4 +1,5 @@
-// k2_replay.cu -- K2: whole-trace replay, one warp per scenario (steps a2-a8).
+// k2_replay.cu -- K2: whole-trace replay (steps a2-a8), one warp segment per
+// scenario.
 //
 // The online serving loop of EdgeServing with exclusive
 // time-division GPU execution, replayed decision by
@@ -16,9 +17,16 @@
 //       arrival if every queue is empty (work-conserving idle, reading Q12).
 //   a9  per-scenario counters (Eq. 2 strict violations after the warmup of
 //       reading Q14); the P95 is K3 (k3_stats.cu).
-// Scenarios are handed out by a device-wide atomic counter (persistent warps)
-// because chain lengths differ by ~4x across rho and tau.
+//
+// Execution model: a warp holds 32/LPS segments; each segment replays one
+// scenario at a time and pulls the next from a device-wide atomic counter as
+// soon as its scenario drains (chain lengths differ ~4x across rho and tau).
+// All segments step in lockstep -- one decision (or one idle jump) per
+// iteration -- with per-segment predicates, so every warp-synchronous
+// primitive is executed by the whole warp.
 #include <cuda_runtime.h>
+
+#include <cstdlib>
 
 #include "decide.cuh"
 
@@ -51,189 +59,246 @@ __device__ __forceinline__ void report(DevStatus *ds, uint32_t code, int64_t ite
   if (atomicCAS(&ds->code, 0u, code) == 0u) ds->item = (unsigned long long)item;
 }
 
-template <int MM>
-__device__ void replay_one(const Lanes<MM> &ln, const uint8_t *sm, const SmemProf &P, const ReplayArgs &a,
-                           int64_t s) {
-  constexpr int GL = Lanes<MM>::GL;
-  const int g = ln.grp;
-  const int M = P.M;
-  uint64_t *st = a.stats + s * ES_NSTAT;
-  const int k = a.cfg_idx ? (int)a.cfg_idx[s] : 0;
-  if (k >= P.ncfg) {
-    if (ln.lane < ES_NSTAT) st[ln.lane] = (ln.lane == ES_ST_STATUS) ? (uint64_t)ES_ERR_ARG : 0ull;
-    if (ln.lane == 0) report(a.dstat, ES_ERR_ARG, s);
-    return;
-  }
-  const SmemCfg C = smem_cfg(sm, P, k);
-  const uint64_t base0 = a.arr_off[s * M];
-  uint64_t qb = 0;
-  uint32_t n = 0;
-  if (g < M) {
-    qb = a.arr_off[s * M + g];
-    n = (uint32_t)(a.arr_off[s * M + g + 1] - qb);
-  }
-  const uint32_t *Aq = a.arrival + qb;
-  const uint32_t total = red_u32(ln.gl == 0 ? n : 0u);
-  uint32_t next_arr = n ? ldg_u32(Aq) : 0xFFFFFFFFu;
-  uint32_t t = __reduce_min_sync(FULL, next_arr);
-  uint32_t head = 0, tail = 0, live = 0, last = 0;
-  uint32_t served = 0, seq = 0;
-  uint32_t status = ES_OK;
-  // uniform counters
-  uint64_t decisions = 0, candidates = 0, infeasible = 0, live_sum = 0, terms = 0;
-  // lane-local counters (reduced at the end)
-  uint32_t completed = 0, viol = 0, cells = 0, maxd = 0;
-  uint64_t sum_lat = 0;
-  const uint32_t mbits = g < M ? P.mask[g] : 0u;
-  const uint32_t nallow = __popc(mbits);
-  while (served < total) {
-    // ---- a2: admission (every arrival with a <= t)
-    bool more = true;
-    while (more) {
-      const uint32_t idx = tail + ln.gl;
-      const uint32_t v = idx < n ? ldg_u32(Aq + idx) : 0xFFFFFFFFu;
-      uint32_t prev = __shfl_up_sync(FULL, v, 1, GL);
-      if (ln.gl == 0) prev = last;
-      const bool bad = idx < n && v < prev;
-      const bool ok = idx < n && v <= t;
-      const unsigned b = ln.gbits(__ballot_sync(FULL, ok));
-      const uint32_t cnt = __popc(b);
-      const uint32_t lv = __shfl_sync(FULL, v, g * GL + (cnt ? cnt - 1 : 0));
-      next_arr = __shfl_sync(FULL, v, g * GL + (cnt < GL ? cnt : GL - 1));
-      if (cnt) last = lv;
-      tail += cnt;
-      if (__any_sync(FULL, bad)) {
-        status = ES_ERR_UNSORTED;
-        break;
-      }
-      more = __any_sync(FULL, cnt == (uint32_t)GL);
-    }
-    if (status) break;
-    uint32_t len = tail - head;
-    if (!__any_sync(FULL, len > 0u)) {  // idle GPU: jump to the next arrival (Q12)
-      t = __reduce_min_sync(FULL, next_arr);
-      continue;
-    }
-    maxd = max(maxd, len);
-    // ---- a3/a4 inputs: head wait, clipped-for-everyone prefix
-    const uint32_t ahead = len ? ldg_u32(Aq + head) : t;
-    const uint32_t wmax = t - ahead;
-    if (live < head) live = head;
-    if (__any_sync(FULL, len > 0u && wmax >= C.x_c)) {
-      bool adv = true;
-      while (adv) {
-        const uint32_t idx = live + ln.gl;
-        const bool pr = idx < tail && (t - ldg_u32(Aq + idx)) >= C.x_c;
-        const uint32_t cnt = __popc(ln.gbits(__ballot_sync(FULL, pr)));
-        live += cnt;
-        adv = __any_sync(FULL, cnt == (uint32_t)GL);
-      }
-    }
-    const uint32_t c = live - head;
-    const Cand cand = cand_params<MM>(ln, P, C, g, len, wmax);
-    const uint32_t hq = head;
-    const uint32_t tt = t;
-    const Decision d = decide<MM>(ln, C, len, c, cand, [&](uint32_t p) { return tt - ldg_u32(Aq + hq + p); });
-    // ---- a8: commit
-    const uint64_t done64 = (uint64_t)t + d.L;
-    if (done64 > 0xFFFFFFFFull) {
-      status = ES_ERR_RANGE;
-      break;
-    }
-    const uint32_t done = (uint32_t)done64;
-    decisions++;
-    const uint32_t ncand = __popc(__ballot_sync(FULL, ln.gl == 0 && len > 0u));
-    const uint32_t nlive = red_u32(ln.gl == 0 ? len - c : 0u);
-    candidates += ncand;
-    live_sum += nlive;
-    terms += (uint64_t)nlive * ncand;
-    if (ln.gl == 0 && len > 0u) cells += nallow;
-    if (!d.feas) infeasible++;
-    const int src = (int)d.m * GL;
-    const uint64_t qb_w = __shfl_sync(FULL, qb, src);
-    const uint32_t head_w = __shfl_sync(FULL, head, src);
-    for (uint32_t j = ln.lane; j < d.B; j += 32) {
-      const uint64_t i = qb_w + head_w + j;
-      const uint32_t T = done - ldg_u32(a.arrival + i);  // Eq. 1: T = w + t
-      if (a.completion) a.completion[i] = done;
-      if (a.exit_used) a.exit_used[i] = (uint8_t)d.e;
-      const uint32_t q = seq + j;
-      a.lat[base0 + q] = T;
-      if (q >= C.warmup) {  // reading Q14
-        completed++;
-        sum_lat += T;
-        viol += T > C.tau ? 1u : 0u;  // Eq. 2, strict
-      }
-    }
-    if (a.dec_cap && ln.lane == 0 && (int64_t)decisions <= a.dec_cap) {
-      const int64_t o = s * a.dec_cap + (int64_t)decisions - 1;
-      if (a.dec_t) a.dec_t[o] = t;
-      if (a.dec_m) a.dec_m[o] = (uint8_t)d.m;
-      if (a.dec_e) a.dec_e[o] = (uint8_t)d.e;
-      if (a.dec_B) a.dec_B[o] = (uint16_t)d.B;
-      if (a.dec_L) a.dec_L[o] = d.L;
-      if (a.dec_S) a.dec_S[o] = d.S;
-      if (a.dec_f) a.dec_f[o] = d.feas ? 1 : 0;
-    }
-    if (g == (int)d.m) head += d.B;
-    seq += d.B;
-    served += d.B;
-    t = done;  // next round on completion
-  }
-  // ---- a9: per-scenario counters
-  completed = red_u32(completed);
-  viol = red_u32(viol);
-  cells = red_u32(cells);
-  maxd = __reduce_max_sync(FULL, maxd);
-  sum_lat = red_u64(sum_lat);
-  if (ln.lane == 0) {
-    st[ES_ST_DECISIONS] = decisions;
-    st[ES_ST_CANDIDATES] = candidates;
-    st[ES_ST_CELLS] = cells;
-    st[ES_ST_COMPLETED] = completed;
-    st[ES_ST_VIOLATIONS] = viol;
-    st[ES_ST_INFEASIBLE] = infeasible;
-    st[ES_ST_MAX_DEPTH] = maxd;
-    st[ES_ST_STATUS] = status;
-    st[ES_ST_SUM_LAT] = sum_lat;
-    st[ES_ST_LIVE] = live_sum;
-    st[ES_ST_TERMS] = terms;
-    if (status) report(a.dstat, status, s);
-  }
-}
-
-template <int MM>
+template <int LPS, int MM>
 __global__ void __launch_bounds__(256) k2_replay(const uint8_t *__restrict__ gimg, ImgLayout lay, ReplayArgs a) {
+  constexpr int GL = Seg<LPS, MM>::GL;
   extern __shared__ __align__(16) uint8_t smem[];
   __shared__ uint64_t mbar;
   stage_image(smem, gimg, lay.bytes, &mbar);
   const SmemProf P = smem_prof(smem, lay);
-  const Lanes<MM> ln;
+  const Seg<LPS, MM> sg;
+  const int g = sg.grp;
+  const int M = P.M;
+  const uint32_t mbits = g < M ? P.mask[g] : 0u;
+  const uint32_t nallow = __popc(mbits);
+
+  // ---- per-segment scenario state (uniform within a segment, per group for queues)
+  bool active = false, exhausted = false;
+  int64_t s = 0;
+  SmemCfg C{};
+  uint64_t base0 = 0, qb = 0;
+  const uint32_t *Aq = a.arrival;
+  uint32_t n = 0, head = 0, tail = 0, live = 0, last = 0, next_arr = 0xFFFFFFFFu;
+  uint32_t t = 0, total = 0, served = 0, seq = 0, status = 0;
+  uint64_t decisions = 0, candidates = 0, infeasible = 0;
+  // lane-local counters (reduced once per scenario)
+  uint32_t completed = 0, viol = 0, cells = 0, maxd = 0;
+  uint64_t sum_lat = 0, live_sum = 0, terms = 0;
+
   for (;;) {
-    unsigned long long s = 0;
-    if (ln.lane == 0) s = atomicAdd(a.work, 1ull);
-    s = __shfl_sync(FULL, s, 0);
-    if ((int64_t)s >= a.n_scen) break;
-    replay_one<MM>(ln, smem, P, a, (int64_t)s);
+    // ---- refill: segments without a scenario fetch the next one
+    const bool need = !active && !exhausted;
+    if (__any_sync(FULL, need)) {
+      unsigned long long got = 0;
+      if (need && sg.sl == 0) got = atomicAdd(a.work, 1ull);
+      got = sg.bcast(got, 0);
+      bool fresh = false;
+      if (need) {
+        if ((int64_t)got >= a.n_scen) exhausted = true;
+        else fresh = true;
+      }
+      int k = 0;
+      uint32_t n_new = 0, a0 = 0xFFFFFFFFu;
+      if (fresh) {
+        s = (int64_t)got;
+        k = a.cfg_idx ? (int)a.cfg_idx[s] : 0;
+        qb = 0;
+        if (k < P.ncfg) {
+          C = smem_cfg(P, k);
+          base0 = a.arr_off[s * M];
+          if (g < M) {
+            qb = a.arr_off[s * M + g];
+            n_new = (uint32_t)(a.arr_off[s * M + g + 1] - qb);
+          }
+        }
+        Aq = a.arrival + qb;
+        if (n_new) a0 = ldg_u32(Aq);
+      }
+      const uint32_t tot = sg.sum(sg.gl == 0 ? n_new : 0u);
+      const uint32_t t0 = sg.vmin(a0);
+      if (fresh) {
+        active = true;
+        n = n_new;
+        next_arr = a0;
+        total = tot;
+        t = t0;
+        head = tail = live = last = 0;
+        served = seq = 0;
+        status = (k < P.ncfg) ? (uint32_t)ES_OK : (uint32_t)ES_ERR_ARG;
+        decisions = candidates = infeasible = 0;
+        completed = viol = cells = maxd = 0;
+        sum_lat = live_sum = terms = 0;
+      }
+    }
+    if (__all_sync(FULL, exhausted)) break;
+
+    // ---- decisions until some segment of the warp drains its scenario
+    for (;;) {
+      const bool run = active && status == ES_OK && served < total;
+      // a2: admission (every arrival with a <= t)
+      const bool pre_ok = run && head < tail;
+      const uint32_t ahead_pre = pre_ok ? ldg_u32(Aq + head) : 0u;  // head arrival, issued early
+      bool more = true;
+      while (more) {
+        const uint32_t idx = tail + sg.gl;
+        const bool valid = run && idx < n;
+        const uint32_t v = valid ? ldg_u32(Aq + idx) : 0xFFFFFFFFu;
+        uint32_t prev = __shfl_up_sync(FULL, v, 1, GL);
+        if (sg.gl == 0) prev = last;
+        const bool ok = valid && v <= t;
+        const unsigned bal = __ballot_sync(FULL, ok);
+        const unsigned badb = __ballot_sync(FULL, valid && v < prev);
+        const uint32_t cnt = __popc(sg.gbits(bal));
+        const uint32_t lv = __shfl_sync(FULL, v, sg.grp * GL + (cnt ? cnt - 1 : 0), LPS);
+        const uint32_t nx = __shfl_sync(FULL, v, sg.grp * GL + (cnt < GL ? cnt : GL - 1), LPS);
+        if (run) {
+          next_arr = nx;
+          if (cnt) last = lv;
+          tail += cnt;
+          if (sg.sbits(badb)) status = ES_ERR_UNSORTED;
+        }
+        more = __any_sync(FULL, run && status == ES_OK && cnt == (uint32_t)GL);
+      }
+      const bool go = run && status == ES_OK;
+      uint32_t len = go ? tail - head : 0u;
+      const bool has = sg.seg_any(len > 0u);
+      if (__any_sync(FULL, go && !has)) {  // idle GPU: jump to the next arrival (Q12)
+        const uint32_t tn = sg.vmin(go ? next_arr : 0xFFFFFFFFu);
+        if (go && !has) t = tn;
+      }
+      const bool dec = go && has;
+      if (!dec) len = 0u;
+      maxd = max(maxd, len);
+      // a3/a4 inputs: head wait, clipped-for-everyone prefix
+      const uint32_t ahead = len == 0u ? t : (pre_ok ? ahead_pre : ldg_u32(Aq + head));
+      const uint32_t wmax = t - ahead;
+      if (live < head) live = head;
+      if (__any_sync(FULL, len > 0u && wmax >= C.x_c)) {
+        bool adv = true;
+        while (adv) {
+          const uint32_t idx = live + sg.gl;
+          const bool pr = len > 0u && idx < tail && (t - ldg_u32(Aq + idx)) >= C.x_c;
+          const uint32_t cnt = __popc(sg.gbits(__ballot_sync(FULL, pr)));
+          live += cnt;
+          adv = __any_sync(FULL, cnt == (uint32_t)GL);
+        }
+      }
+      const uint32_t c = len ? live - head : 0u;
+      const Cand cand = cand_params<LPS, MM>(sg, P, C, len, wmax);
+      const uint32_t tt = t;
+      const uint32_t *Ah = Aq + head;
+      const Decision d =
+          decide<LPS, MM>(sg, P, C, len, c, wmax, cand, [&](uint32_t p) { return tt - ldg_u32(Ah + p); });
+      const uint32_t ncand = __popc(sg.sbits(__ballot_sync(FULL, sg.gl == 0 && len > 0u)));
+      // a8: commit
+      const int src = (int)(d.m & (MM - 1)) * GL;
+      const uint64_t qb_w = sg.bcast(qb, src);
+      const uint32_t head_w = sg.bcast(head, src);
+      if (dec) {
+        const uint64_t done64 = (uint64_t)t + d.L;
+        if (done64 > 0xFFFFFFFFull) {
+          status = ES_ERR_RANGE;
+        } else {
+          const uint32_t done = (uint32_t)done64;
+          decisions++;
+          candidates += ncand;
+          if (!d.feas) infeasible++;
+          if (sg.gl == 0 && len > 0u) {
+            cells += nallow;
+            live_sum += len - c;
+            terms += (uint64_t)(len - c) * ncand;
+          }
+          for (uint32_t j = sg.sl; j < d.B; j += LPS) {
+            const uint64_t i = qb_w + head_w + j;
+            const uint32_t T = done - ldg_u32(a.arrival + i);  // Eq. 1: T = w + t
+            if (a.completion) a.completion[i] = done;
+            if (a.exit_used) a.exit_used[i] = (uint8_t)d.e;
+            const uint32_t q = seq + j;
+            a.lat[base0 + q] = T;
+            if (q >= C.warmup) {  // reading Q14
+              completed++;
+              sum_lat += T;
+              viol += T > C.tau ? 1u : 0u;  // Eq. 2, strict
+            }
+          }
+          if (a.dec_cap && sg.sl == 0 && (int64_t)decisions <= a.dec_cap) {
+            const int64_t o = s * a.dec_cap + (int64_t)decisions - 1;
+            if (a.dec_t) a.dec_t[o] = t;
+            if (a.dec_m) a.dec_m[o] = (uint8_t)d.m;
+            if (a.dec_e) a.dec_e[o] = (uint8_t)d.e;
+            if (a.dec_B) a.dec_B[o] = (uint16_t)d.B;
+            if (a.dec_L) a.dec_L[o] = d.L;
+            if (a.dec_S) a.dec_S[o] = d.S;
+            if (a.dec_f) a.dec_f[o] = d.feas ? 1 : 0;
+          }
+          if (g == (int)d.m) head += d.B;
+          seq += d.B;
+          served += d.B;
+          t = done;  // next round on completion
+        }
+      }
+      if (__any_sync(FULL, active && (served >= total || status != ES_OK))) break;
+    }
+
+    // ---- a9: drained (or failed) scenarios write their counters
+    const bool fin = active && (served >= total || status != ES_OK);
+    const uint32_t r_comp = sg.sum(completed), r_viol = sg.sum(viol), r_cells = sg.sum(cells);
+    const uint32_t r_maxd = sg.vmax(maxd);
+    const uint64_t r_sum = sg.sum64(sum_lat), r_live = sg.sum64(live_sum), r_terms = sg.sum64(terms);
+    if (fin) {
+      if (sg.sl == 0) {
+        uint64_t *st = a.stats + s * ES_NSTAT;
+        st[ES_ST_DECISIONS] = decisions;
+        st[ES_ST_CANDIDATES] = candidates;
+        st[ES_ST_CELLS] = r_cells;
+        st[ES_ST_COMPLETED] = r_comp;
+        st[ES_ST_VIOLATIONS] = r_viol;
+        st[ES_ST_INFEASIBLE] = infeasible;
+        st[ES_ST_MAX_DEPTH] = r_maxd;
+        st[ES_ST_STATUS] = status;
+        st[ES_ST_SUM_LAT] = r_sum;
+        st[ES_ST_LIVE] = r_live;
+        st[ES_ST_TERMS] = r_terms;
+        if (status) report(a.dstat, status, s);
+      }
+      active = false;
+    }
   }
 }
 
-template <int MM>
-cudaError_t launch_mm(const uint8_t *img, const ImgLayout &lay, const ReplayArgs &a, cudaStream_t st, int sms) {
-  auto kern = k2_replay<MM>;
+template <int LPS, int MM>
+cudaError_t launch_t(const uint8_t *img, const ImgLayout &lay, const ReplayArgs &a, cudaStream_t st, int sms) {
+  auto kern = k2_replay<LPS, MM>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lay.bytes);
   if (e != cudaSuccess) return e;
   int occ = 0;
   e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 256, lay.bytes);
   if (e != cudaSuccess) return e;
   if (occ < 1) return cudaErrorInvalidConfiguration;
-  const int64_t warps_needed = a.n_scen;
-  int64_t blocks = (warps_needed + 7) / 8;
+  constexpr int SEG_PER_BLOCK = 256 / LPS;
+  int64_t blocks = (a.n_scen + SEG_PER_BLOCK - 1) / SEG_PER_BLOCK;
   const int64_t cap = (int64_t)sms * occ;
   if (blocks > cap) blocks = cap;
   if (blocks < 1) blocks = 1;
   kern<<<(unsigned)blocks, 256, lay.bytes, st>>>(img, lay, a);
   return cudaGetLastError();
+}
+
+template <int LPS>
+cudaError_t launch_lps(const uint8_t *img, const ImgLayout &lay, const ReplayArgs &a, cudaStream_t st, int sms) {
+  if (lay.M <= 2) return launch_t<LPS, 2>(img, lay, a, st, sms);
+  if (lay.M <= 4) return launch_t<LPS, 4>(img, lay, a, st, sms);
+  return launch_t<LPS, 8>(img, lay, a, st, sms);
+}
+
+// lanes per scenario: ES_LPS overrides; default 16 for M <= 4, 32 above
+int choose_lps(const ImgLayout &lay) {
+  const char *env = getenv("ES_LPS");
+  if (env) {
+    int v = atoi(env);
+    if (v == 8 || v == 16 || v == 32) return v;
+  }
+  return lay.M <= 4 ? 16 : 32;
 }
 
 }  // namespace
@@ -263,9 +328,10 @@ cudaError_t launch_replay(const uint8_t *img, const ImgLayout &lay, const es_tra
   cudaError_t e = cudaMemsetAsync(work_ctr, 0, sizeof(unsigned long long), st);
   if (e != cudaSuccess) return e;
   *n_launch += 1;
-  if (lay.M <= 2) return launch_mm<2>(img, lay, a, st, sms);
-  if (lay.M <= 4) return launch_mm<4>(img, lay, a, st, sms);
-  return launch_mm<8>(img, lay, a, st, sms);
+  const int lps = choose_lps(lay);
+  if (lps == 8 && lay.M <= 8) return launch_lps<8>(img, lay, a, st, sms);
+  if (lps == 16) return launch_lps<16>(img, lay, a, st, sms);
+  return launch_lps<32>(img, lay, a, st, sms);
 }
 
 }  // namespace es

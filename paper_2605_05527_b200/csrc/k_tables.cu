@@ -152,6 +152,9 @@ __global__ void k_build_tables(uint8_t *img, ImgLayout lay) {
     }
     uint32_t r = (S - tau % S) % S;
     uint32_t nA = ((x_c - 1u + r) >> SBITS) + 1u;
+    uint32_t lmax = 0;
+    for (int i = 0; i < lay.M * lay.E * lay.nb; ++i) lmax = lat[i] > lmax ? lat[i] : lmax;
+    rec->fast_lim = x_c > lmax ? x_c - lmax : 0u;
     rec->x_c = x_c;
     rec->r = r;
     rec->nA = nA;
