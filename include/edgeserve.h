@@ -53,7 +53,8 @@ typedef enum {
   ES_ERR_CUDA = 6,             /* CUDA runtime error (message has the name)     */
   ES_ERR_OOM = 7,              /* device allocation failed                      */
   ES_ERR_UNSORTED = 8,         /* arrivals not sorted within a (scen, model)    */
-  ES_ERR_NUMERIC = 9           /* a table value too close to an integer to floor */
+  ES_ERR_NUMERIC = 9,          /* a table value too close to an integer to floor */
+  ES_ERR_INTERNAL = 10         /* a kernel invariant failed (e.g. replay made no progress) */
 } es_status;
 
 #if defined(__GNUC__)

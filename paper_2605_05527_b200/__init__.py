@@ -17,7 +17,7 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libedgeserve.so")
+LIB_PATH = os.environ.get("ES_LIB") or os.path.join(_HERE, "libedgeserve.so")
 
 ES_NSTAT = 11
 ES_NGSTAT = 7
@@ -27,7 +27,7 @@ STAT_COLS = ["decisions", "candidates", "cells", "completed", "violations", "inf
 GROUP_COLS = ["decisions", "candidates", "cells", "completed", "violations", "infeasible", "sum_lat"]
 STATUS = {0: "ES_OK", 1: "ES_ERR_ARG", 2: "ES_ERR_PROFILE_GRID", 3: "ES_ERR_PROFILE_MONOTONE",
           4: "ES_ERR_OUT_OF_GRID", 5: "ES_ERR_RANGE", 6: "ES_ERR_CUDA", 7: "ES_ERR_OOM",
-          8: "ES_ERR_UNSORTED", 9: "ES_ERR_NUMERIC"}
+          8: "ES_ERR_UNSORTED", 9: "ES_ERR_NUMERIC", 10: "ES_ERR_INTERNAL"}
 EXPORTS = ["es_last_error", "es_version", "es_load_profile", "es_free_profile", "es_get_tables",
            "es_score_candidates", "es_replay_traces", "es_scen_p95", "es_replay_traces_host", "es_group_accumulate",
            "es_group_hist", "es_group_p95_select", "es_device_status", "es_launch_count"]

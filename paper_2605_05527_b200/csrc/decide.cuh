@@ -128,6 +128,24 @@ __device__ __forceinline__ void stage_image(uint8_t *smem, const uint8_t *gimg, 
 
 __device__ __forceinline__ constexpr unsigned low_mask(int n) { return n >= 32 ? FULL : ((1u << n) - 1u); }
 
+// Full-warp REDUX as volatile PTX: the compiler must not sink it into a
+// lane-dependent branch (only the full warp may execute redux.sync).
+__device__ __forceinline__ uint32_t redux_add(uint32_t v) {
+  uint32_t r;
+  asm volatile("redux.sync.add.u32 %0, %1, 0xffffffff;" : "=r"(r) : "r"(v));
+  return r;
+}
+__device__ __forceinline__ uint32_t redux_min(uint32_t v) {
+  uint32_t r;
+  asm volatile("redux.sync.min.u32 %0, %1, 0xffffffff;" : "=r"(r) : "r"(v));
+  return r;
+}
+__device__ __forceinline__ uint32_t redux_max(uint32_t v) {
+  uint32_t r;
+  asm volatile("redux.sync.max.u32 %0, %1, 0xffffffff;" : "=r"(r) : "r"(v));
+  return r;
+}
+
 // Lane roles inside a warp: 32/LPS segments, MM groups of GL lanes each.
 // Reductions use compile-time-constant masks (a runtime mask makes ptxas emit
 // a collective loop): REDUX over the full warp when LPS == 32, xor-shuffle
@@ -155,44 +173,56 @@ struct Seg {
     return LPS == 32 ? ballot : (ballot >> seg_base) & low_mask(LPS);
   }
   __device__ __forceinline__ bool seg_any(bool p) const { return sbits(__ballot_sync(FULL, p)) != 0u; }
+  static constexpr int SPW = 32 / LPS;  // segments per warp
+  // Segment reductions: one full-mask REDUX per segment with the other
+  // segments' lanes contributing the identity, then each lane keeps its own.
   __device__ __forceinline__ uint32_t sum(uint32_t v) const {
+    __syncwarp();  // segments may arrive from divergent paths: reconverge first
     if constexpr (LPS == 32) {
-      return __reduce_add_sync(FULL, v);
+      return redux_add(v);
     } else {
+      uint32_t r = 0;
 #pragma unroll
-      for (int o = LPS / 2; o >= 1; o >>= 1) v += __shfl_xor_sync(FULL, v, o, LPS);
-      return v;
+      for (int k = 0; k < SPW; ++k) {
+        const uint32_t x = redux_add(seg == k ? v : 0u);
+        if (seg == k) r = x;
+      }
+      return r;
     }
   }
   __device__ __forceinline__ uint32_t vmin(uint32_t v) const {
+    __syncwarp();  // segments may arrive from divergent paths: reconverge first
     if constexpr (LPS == 32) {
-      return __reduce_min_sync(FULL, v);
+      return redux_min(v);
     } else {
+      uint32_t r = 0;
 #pragma unroll
-      for (int o = LPS / 2; o >= 1; o >>= 1) v = min(v, __shfl_xor_sync(FULL, v, o, LPS));
-      return v;
+      for (int k = 0; k < SPW; ++k) {
+        const uint32_t x = redux_min(seg == k ? v : 0xFFFFFFFFu);
+        if (seg == k) r = x;
+      }
+      return r;
     }
   }
   __device__ __forceinline__ uint32_t vmax(uint32_t v) const {
+    __syncwarp();  // segments may arrive from divergent paths: reconverge first
     if constexpr (LPS == 32) {
-      return __reduce_max_sync(FULL, v);
+      return redux_max(v);
     } else {
+      uint32_t r = 0;
 #pragma unroll
-      for (int o = LPS / 2; o >= 1; o >>= 1) v = max(v, __shfl_xor_sync(FULL, v, o, LPS));
-      return v;
+      for (int k = 0; k < SPW; ++k) {
+        const uint32_t x = redux_max(seg == k ? v : 0u);
+        if (seg == k) r = x;
+      }
+      return r;
     }
   }
-  // exact segment sum of u64 values < 2^51 each (24 | 27-bit halves for REDUX)
+  // exact segment sum of u64 values < 2^51 each (24 | 27-bit halves per REDUX)
   __device__ __forceinline__ uint64_t sum64(uint64_t v) const {
-    if constexpr (LPS == 32) {
-      const uint32_t lo = (uint32_t)(v & 0xFFFFFFu);
-      const uint32_t hi = (uint32_t)(v >> 24);
-      return ((uint64_t)__reduce_add_sync(FULL, hi) << 24) + (uint64_t)__reduce_add_sync(FULL, lo);
-    } else {
-#pragma unroll
-      for (int o = LPS / 2; o >= 1; o >>= 1) v += __shfl_xor_sync(FULL, v, o, LPS);
-      return v;
-    }
+    const uint32_t lo = (uint32_t)(v & 0xFFFFFFu);
+    const uint32_t hi = (uint32_t)(v >> 24);
+    return ((uint64_t)sum(hi) << 24) + (uint64_t)sum(lo);
   }
   // exact group sum of u64 values
   __device__ __forceinline__ uint64_t gsum64(uint64_t v) const {
@@ -226,6 +256,21 @@ __device__ __forceinline__ Cand cand_params(const Seg<LPS, MM> &sg, const SmemPr
   const uint32_t mbits = P.mask[gg];
   const uint32_t *row = P.lat + (size_t)gg * P.E * P.nb + bi;  // row[e * nb]
   unsigned bits = 0;
+  if (P.E <= GL) {  // warp-uniform: one exit per lane, L and H fetched in parallel
+    const int e = sg.gl < P.E ? sg.gl : 0;
+    const uint32_t Le = row[e * P.nb];
+    const uint64_t He = reinterpret_cast<const uint64_t *>(P.sm + C.off_H)[((size_t)gg * P.E + e) * P.nb + bi];
+    const bool ok = sg.gl < P.E && ((mbits >> sg.gl) & 1u) && (uint64_t)wmax + Le <= (uint64_t)C.tau;
+    bits = sg.gbits(__ballot_sync(FULL, ok));
+    k.feas = bits != 0u;
+    k.e = k.feas ? 31u - __clz(bits) : (uint32_t)(__ffs(mbits) - 1);
+    const int src = sg.grp * GL + (int)k.e;
+    k.L = __shfl_sync(FULL, Le, src, LPS);
+    k.H = __shfl_sync(FULL, He, src, LPS);
+    k.thr = k.L < C.x_c ? C.x_c - k.L : 0u;
+    if (k.L >= C.x_c) k.H = 0ull;
+    return k;
+  }
 #pragma unroll
   for (int e0 = 0; e0 < MAXE; e0 += GL) {  // compile-time trip count, E <= MAXE
     if (e0 >= P.E) break;                 // warp-uniform
@@ -256,13 +301,30 @@ __device__ __forceinline__ Decision finish_decision(const Seg<LPS, MM> &sg, cons
                                                    uint32_t mkey) {
   constexpr int GL = Seg<LPS, MM>::GL;
   const uint64_t S_own = Sq;
+  constexpr uint64_t LIM = 1ull << 61;
+  if (!__any_sync(FULL, mkey != 0xFFu && Sq >= LIM)) {
+    // key = S * 8 + m orders exactly like (S, m) while S < 2^61; empty -> max
+    uint64_t key = mkey == 0xFFu ? ~0ull : ((Sq << 3) | mkey);
 #pragma unroll
-  for (int o = GL; o < LPS; o <<= 1) {
-    const uint64_t So = __shfl_xor_sync(FULL, Sq, o, LPS);
-    const uint32_t mo = __shfl_xor_sync(FULL, mkey, o, LPS);
-    if (So < Sq || (So == Sq && mo < mkey)) {
-      Sq = So;
-      mkey = mo;
+    for (int o = GL; o < LPS; o <<= 1) {
+      const uint64_t ko = __shfl_xor_sync(FULL, key, o, LPS);
+      key = ko < key ? ko : key;
+    }
+    if (key != ~0ull) {
+      Sq = key >> 3;
+      mkey = (uint32_t)(key & 7u);
+    } else {
+      mkey = 0xFFu;
+    }
+  } else {
+#pragma unroll
+    for (int o = GL; o < LPS; o <<= 1) {
+      const uint64_t So = __shfl_xor_sync(FULL, Sq, o, LPS);
+      const uint32_t mo = __shfl_xor_sync(FULL, mkey, o, LPS);
+      if (So < Sq || (So == Sq && mo < mkey)) {
+        Sq = So;
+        mkey = mo;
+      }
     }
   }
   Decision d;
@@ -315,6 +377,7 @@ __device__ __forceinline__ Decision decide_general(const Seg<LPS, MM> &sg, const
       else U[m] += gw;
     }
   }
+  __syncwarp();
   // exact segment reductions; each group keeps its own candidate's sums
   uint32_t k_own = 0u;
   uint64_t u_own = 0ull;
@@ -367,6 +430,7 @@ __device__ __forceinline__ Decision decide(const Seg<LPS, MM> &sg, const SmemPro
       tot += gw;
       if (p < Bown) srv += gw;
     }
+    __syncwarp();
     tot = sg.sum64(tot);
     srv = sg.gsum64(srv);
     if (len) {

@@ -79,7 +79,7 @@ __global__ void __launch_bounds__(256) k2_replay(const uint8_t *__restrict__ gim
   uint64_t base0 = 0, qb = 0;
   const uint32_t *Aq = a.arrival;
   uint32_t n = 0, head = 0, tail = 0, live = 0, last = 0, next_arr = 0xFFFFFFFFu;
-  uint32_t t = 0, total = 0, served = 0, seq = 0, status = 0;
+  uint32_t t = 0, total = 0, served = 0, seq = 0, status = 0, iters = 0;
   uint64_t decisions = 0, candidates = 0, infeasible = 0;
   // lane-local counters (reduced once per scenario)
   uint32_t completed = 0, viol = 0, cells = 0, maxd = 0;
@@ -123,7 +123,7 @@ __global__ void __launch_bounds__(256) k2_replay(const uint8_t *__restrict__ gim
         total = tot;
         t = t0;
         head = tail = live = last = 0;
-        served = seq = 0;
+        served = seq = iters = 0;
         status = (k < P.ncfg) ? (uint32_t)ES_OK : (uint32_t)ES_ERR_ARG;
         decisions = candidates = infeasible = 0;
         completed = viol = cells = maxd = 0;
@@ -134,6 +134,8 @@ __global__ void __launch_bounds__(256) k2_replay(const uint8_t *__restrict__ gim
 
     // ---- decisions until some segment of the warp drains its scenario
     for (;;) {
+      // progress guard: each iteration serves >= 1 request or jumps to an arrival
+      if (active && status == ES_OK && ++iters > 2u * total + 4u) status = ES_ERR_INTERNAL;
       const bool run = active && status == ES_OK && served < total;
       // a2: admission (every arrival with a <= t)
       const bool pre_ok = run && head < tail;
