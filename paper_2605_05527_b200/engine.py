@@ -69,3 +69,20 @@ def replay_group_stats(prof, dtr, n_groups, full=False, group=None, stream=None,
                            full=full, stream=stream)
     counts, p95 = group_merge(prof, dtr, out, n_groups, group=group, stream=stream)
     return out, counts, p95
+
+
+def shard_ids(n_total, rank, world):
+    """Contiguous scenario block of `rank` when n_total scenarios are split over
+    `world` ranks (strong scaling); the last ranks may get one fewer."""
+    base, extra = divmod(int(n_total), int(world))
+    lo = rank * base + min(rank, extra)
+    hi = lo + base + (1 if rank < extra else 0)
+    return np.arange(lo, hi, dtype=np.int64)
+
+
+def weak_ids(per_rank, rank):
+    """Weak scaling: rank r replays scenarios [r S, (r+1) S) of the config's sequence."""
+    return np.arange(rank * per_rank, (rank + 1) * per_rank, dtype=np.int64)
+
+
+RADIX_LEVELS = ((20, 12), (8, 12), (0, 8))  # (shift, bits) of the 3 group-P95 selection levels

@@ -1,0 +1,12 @@
+# Full bench line + ncu launch list + one ncu --set full capture of K2 (round artefacts)
+R=${R:-r01}
+timeout 300 python bench.py --steps 50 --warmup 5 > gpurun_out/bench_$R.json 2> gpurun_out/bench_$R.err
+tail -2 gpurun_out/bench_$R.err
+timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_$R.csv \
+  python bench.py --steps 2 --warmup 1 --ncu > /dev/null 2>&1
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:k2_replay -s 1 -c 1 \
+  -o gpurun_out/prof_k2_$R python bench.py --steps 1 --warmup 1 --ncu > /dev/null 2>&1
+timeout 600 ncu --set full --clock-control none -k regex:k3_scen_p95 -s 1 -c 1 \
+  -o gpurun_out/prof_k3_$R python bench.py --steps 1 --warmup 1 --ncu > /dev/null 2>&1
+timeout 200 python bench.py --impl reference --steps 3 --warmup 1 > gpurun_out/bench_ref_$R.json 2>&1
+ls gpurun_out

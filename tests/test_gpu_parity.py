@@ -279,3 +279,49 @@ def test_determinism_repeat():
     b = run_k2(w)
     for k in ["stats", "p95", "completion", "exit", "latency"]:
         assert np.array_equal(a[k], b[k])
+
+
+def test_group_merge_rank_count_invariance():
+    """Split the scenarios over W = 1, 2, 4, 8 emulated ranks on one GPU: each
+    shard replays and histograms its own scenarios; the per-shard u64 buffers
+    are summed (what all_reduce(sum) does) between the radix levels.  Counters
+    and P95 must be bit-identical for every W and equal the oracle's."""
+    from paper_2605_05527_b200 import engine
+    n, G = 40, 13
+    w = inputs.workload("cfg2", scen_ids=np.arange(n), n_req=900)
+    h = es.es_load_profile(w.profile, w.cfgs)
+    o = oracle.replay_batch(w.profile, w.cfgs, w.traces, nthreads=8)
+    oc, op = oracle.group_stats(w.traces, o, w.cfgs, G)
+    results = []
+    for W in (1, 2, 4, 8):
+        shards = []
+        for r in range(W):
+            sub = inputs.workload("cfg2", scen_ids=engine.shard_ids(n, r, W), n_req=900)
+            d = es.upload_traces(sub.traces, DEV)
+            out = es.es_replay_traces(h, d["arr_off"], d["arrival"], d["cfg_idx"], d["group_id"], full=False)
+            shards.append((d, out))
+        bufs = []
+        for d, out in shards:
+            buf = torch.zeros(G * 7 + G * 4096, dtype=torch.uint64, device=DEV)
+            es.es_group_accumulate(h, d["arr_off"], d["arrival"], out, G, buf[:G * 7], buf[G * 7:], d["cfg_idx"],
+                                   d["group_id"])
+            bufs.append(buf)
+        tot = bufs[0].view(torch.int64).clone()
+        for b in bufs[1:]:
+            tot += b.view(torch.int64)
+        tot = tot.view(torch.uint64)
+        counts, hist = tot[:G * 7], tot[G * 7:]
+        state = torch.zeros(2 * G, dtype=torch.uint64, device=DEV)
+        es.es_group_p95_select(G, 0, counts, hist, state)
+        for level in (1, 2):
+            acc = torch.zeros(G * 4096, dtype=torch.int64, device=DEV)
+            for d, out in shards:
+                hl = torch.empty(G * 4096, dtype=torch.uint64, device=DEV)
+                es.es_group_hist(h, d["arr_off"], d["arrival"], out, G, level, state, hl, d["cfg_idx"], d["group_id"])
+                acc += hl.view(torch.int64)
+            es.es_group_p95_select(G, level, counts, acc.view(torch.uint64), state)
+        torch.cuda.synchronize()
+        results.append((np_of(counts).reshape(G, 7), np_of(state).reshape(G, 2)[:, 0]))
+    for c, p in results:
+        assert np.array_equal(c, oc)
+        assert np.array_equal(p.astype(np.uint32), op)
