@@ -215,8 +215,9 @@ def main():
         if record:
             b.record(stream)
             ev_k2.append((a, b))
-        es.es_scen_p95(h, dtr["arr_off"], dtr["arrival"], out, dtr["cfg_idx"], stream=stream)
-        return engine.group_merge(h, dtr, out, G, group=pg if world > 1 else False, stream=stream)
+        # K3 (per-scenario P95) fused with the level-0 group histogram, then the
+        # all_reduce'd radix levels of the exact group P95
+        return engine.group_merge(h, dtr, out, G, group=pg if world > 1 else False, stream=stream, with_p95=True)
 
     for _ in range(max(args.warmup, 1)):
         counts, p95g = step(False)
@@ -253,7 +254,7 @@ def main():
     if world > 1:
         dist.barrier()
     clocks = sampler.stop() if sampler else None
-    launches = h.launches - l0 + 3 * args.steps  # + the three group-select kernels per step
+    launches = h.launches - l0 + 4 * args.steps  # + the four group-select kernels per step
     ms = t0.elapsed_time(t1)
     k2_ms = [a.elapsed_time(b) for a, b in ev_k2]
     tt = torch.tensor([ms, float(decisions_rank), float(cand_rank)], dtype=torch.float64, device=dev)

@@ -236,30 +236,44 @@ ES_API es_status es_replay_traces_host(es_profile *prof, const es_traces *host_t
 
 /*
  * Accumulate (+=) per-group counters [n_groups][ES_NGSTAT] and the level-0
- * latency histogram [n_groups][4096] (bin = T >> 20) over post-warmup
- * requests of every scenario with status OK.  Buffers are device u64 and must
- * be zeroed by the caller before the first call.  Integer sums: an
+ * (coarse) latency histogram [n_groups][4096], bin = min(T >> 12, 4095)
+ * (4.096 ms bins, 4095 = overflow T >= 16.77 s), over the post-warmup requests
+ * of every scenario with status OK.  Buffers are device u64 and must be
+ * zeroed by the caller before the first call.  Integer sums: an
  * all_reduce(sum) across ranks gives bit-identical results for any rank count.
  */
 ES_API es_status es_group_accumulate(const es_profile *prof, const es_traces *traces,
-                              const es_replay_out *out, uint32_t n_groups, uint64_t *group_counts,
-                              uint64_t *hist0, es_stream stream);
+                                     const es_replay_out *out, uint32_t n_groups, uint64_t *group_counts,
+                                     uint64_t *hist0, es_stream stream);
 
 /*
- * Exact group P95 by three-level radix selection (levels 0, 1, 2 select bits
- * [20,32), [8,20), [0,8) of T).  Call order per level L (all device pointers):
- *   L == 0: es_group_p95_select(0, counts, hist0, state)   (after all_reduce of counts+hist0)
- *   L == 1: es_group_hist(1, state, hist1) -> all_reduce -> es_group_p95_select(1, ...)
- *   L == 2: es_group_hist(2, state, hist2) -> all_reduce -> es_group_p95_select(2, ...)
- * state is u64 [n_groups][2] = {selected prefix, residual rank}; after level 2
- * state[g][0] is the nearest-rank P95 of group g (0 for an empty group).
- * es_group_hist overwrites hist (no need to zero).
+ * K3 fused with es_group_accumulate: per-scenario P95 into out->scen_p95_us
+ * (if non-NULL) and, if group_counts != NULL, the group counters and level-0
+ * histogram -- one pass over the latencies instead of two.
+ */
+ES_API es_status es_scen_stats(const es_profile *prof, const es_traces *traces, es_replay_out *out,
+                               uint32_t n_groups, uint64_t *group_counts, uint64_t *hist0, es_stream stream);
+
+/*
+ * Exact group P95 by radix selection on digits that are identical on every
+ * rank (so histograms can be summed across ranks before each selection):
+ *   level 0: coarse bin min(T >> 12, 4095)        (es_group_accumulate / es_scen_stats)
+ *   level 1: T & 0xFFF inside the coarse bin       -> the exact P95 (normal case)
+ *            or, for a group whose P95 lies in the overflow bin, T >> 20
+ *   level 2: (T >> 8) & 0xFFF (overflow groups only)
+ *   level 3: T & 0xFF          (overflow groups only)
+ * Call order: [all_reduce counts + hist0] -> es_group_p95_select(0); then for
+ * level 1, 2, 3: es_group_hist(level) -> [all_reduce hist] ->
+ * es_group_p95_select(level).  Levels 2 and 3 are no-ops unless some group is
+ * in the overflow bin.  state is u64 [n_groups][2]; after level 3 (or level 1
+ * when no group overflows) state[g][0] is the nearest-rank P95 of group g (0
+ * for an empty group).  es_group_hist overwrites hist (no need to zero).
  */
 ES_API es_status es_group_hist(const es_profile *prof, const es_traces *traces, const es_replay_out *out,
-                        uint32_t n_groups, int32_t level, const uint64_t *state, uint64_t *hist,
-                        es_stream stream);
+                               uint32_t n_groups, int32_t level, const uint64_t *state, uint64_t *hist,
+                               es_stream stream);
 ES_API es_status es_group_p95_select(uint32_t n_groups, int32_t level, const uint64_t *group_counts,
-                              const uint64_t *hist, uint64_t *state, es_stream stream);
+                                     const uint64_t *hist, uint64_t *state, es_stream stream);
 
 /*
  * Synchronise `stream` and report the first device-side error recorded by any

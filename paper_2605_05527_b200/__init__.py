@@ -29,7 +29,8 @@ STATUS = {0: "ES_OK", 1: "ES_ERR_ARG", 2: "ES_ERR_PROFILE_GRID", 3: "ES_ERR_PROF
           4: "ES_ERR_OUT_OF_GRID", 5: "ES_ERR_RANGE", 6: "ES_ERR_CUDA", 7: "ES_ERR_OOM",
           8: "ES_ERR_UNSORTED", 9: "ES_ERR_NUMERIC", 10: "ES_ERR_INTERNAL"}
 EXPORTS = ["es_last_error", "es_version", "es_load_profile", "es_free_profile", "es_get_tables",
-           "es_score_candidates", "es_replay_traces", "es_scen_p95", "es_replay_traces_host", "es_group_accumulate",
+           "es_score_candidates", "es_replay_traces", "es_scen_p95", "es_scen_stats", "es_replay_traces_host",
+           "es_group_accumulate",
            "es_group_hist", "es_group_p95_select", "es_device_status", "es_launch_count"]
 
 P = ctypes.c_void_p
@@ -91,6 +92,7 @@ def lib():
             "es_score_candidates": [P, P, P, P],
             "es_replay_traces": [P, P, P, P],
             "es_scen_p95": [P, P, P, P],
+            "es_scen_stats": [P, P, P, u32, P, P, P],
             "es_replay_traces_host": [P, P, P, P],
             "es_group_accumulate": [P, P, P, u32, P, P, P],
             "es_group_hist": [P, P, P, u32, i32, P, P, P],
@@ -251,6 +253,17 @@ def es_scen_p95(prof: Profile, arr_off, arrival, out, cfg_idx=None, stream=None)
     tr = _traces_struct(n, arr_off, arrival, cfg_idx, None)
     ro = _out_struct(out)
     _check(lib().es_scen_p95(prof.handle, ctypes.byref(tr), ctypes.byref(ro), _stream(stream)))
+    return out
+
+
+def es_scen_stats(prof: Profile, arr_off, arrival, out, n_groups=0, counts=None, hist0=None, cfg_idx=None,
+                  group_id=None, p95=True, stream=None):
+    """K3 fused with the level-0 group accumulation (one pass over latencies)."""
+    n = (arr_off.numel() - 1) // prof.M
+    tr = _traces_struct(n, arr_off, arrival, cfg_idx, group_id)
+    ro = _out_struct(out, p95)
+    _check(lib().es_scen_stats(prof.handle, ctypes.byref(tr), ctypes.byref(ro), ctypes.c_uint32(n_groups),
+                               _ptr(counts), _ptr(hist0), _stream(stream)))
     return out
 
 

@@ -403,11 +403,25 @@ es_status es_group_accumulate(const es_profile *p, const es_traces *tr, const es
   return ES_OK;
 }
 
+es_status es_scen_stats(const es_profile *p, const es_traces *tr, es_replay_out *out, uint32_t n_groups,
+                        uint64_t *counts, uint64_t *hist0, es_stream stream) {
+  if (!p || !tr || !out) return fail(ES_ERR_ARG, "null argument");
+  if (tr->n_scen <= 0) return tr->n_scen == 0 ? ES_OK : fail(ES_ERR_ARG, "n_scen < 0");
+  if (!tr->arr_off || !out->latency_us || !out->scen_stats) return fail(ES_ERR_ARG, "null arr_off / latency / stats");
+  if (counts && (!hist0 || n_groups == 0)) return fail(ES_ERR_ARG, "group outputs need hist0 and n_groups > 0");
+  DeviceGuard guard(p->device);
+  CK(launch_stats_fused(p->d_img, p->lay, *tr, *out, counts ? n_groups : 0u, counts, hist0, (cudaStream_t)stream,
+                        p->sms),
+     "k3_stats");
+  const_cast<es_profile *>(p)->launches++;
+  return ES_OK;
+}
+
 es_status es_group_hist(const es_profile *p, const es_traces *tr, const es_replay_out *out, uint32_t n_groups,
                         int32_t level, const uint64_t *state, uint64_t *hist, es_stream stream) {
   if (!p || !tr || !out || !state || !hist || !out->latency_us || !out->scen_stats)
     return fail(ES_ERR_ARG, "null argument");
-  if (level != 1 && level != 2) return fail(ES_ERR_ARG, "es_group_hist level %d (1 or 2)", level);
+  if (level < 1 || level > 3) return fail(ES_ERR_ARG, "es_group_hist level %d (1..3)", level);
   if (n_groups == 0) return fail(ES_ERR_ARG, "n_groups == 0");
   DeviceGuard guard(p->device);
   if (tr->n_scen <= 0) {
@@ -423,7 +437,7 @@ es_status es_group_hist(const es_profile *p, const es_traces *tr, const es_repla
 es_status es_group_p95_select(uint32_t n_groups, int32_t level, const uint64_t *counts, const uint64_t *hist,
                               uint64_t *state, es_stream stream) {
   if (!hist || !state || (level == 0 && !counts)) return fail(ES_ERR_ARG, "null argument");
-  if (level < 0 || level > 2) return fail(ES_ERR_ARG, "level %d", level);
+  if (level < 0 || level > 3) return fail(ES_ERR_ARG, "level %d", level);
   if (n_groups == 0) return fail(ES_ERR_ARG, "n_groups == 0");
   CK(launch_group_select(n_groups, level, counts, hist, state, (cudaStream_t)stream), "k_group_select");
   return ES_OK;

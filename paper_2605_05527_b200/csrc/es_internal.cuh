@@ -54,6 +54,9 @@ cudaError_t launch_replay(const uint8_t *img, const ImgLayout &lay, const es_tra
                           cudaStream_t st, int sms, int *n_launch);
 cudaError_t launch_scen_p95(const uint8_t *img, const ImgLayout &lay, const es_traces &tr,
                             const es_replay_out &out, cudaStream_t st, int sms);
+cudaError_t launch_stats_fused(const uint8_t *img, const ImgLayout &lay, const es_traces &tr,
+                               const es_replay_out &out, uint32_t n_groups, uint64_t *counts, uint64_t *hist0,
+                               cudaStream_t st, int sms);
 cudaError_t launch_group_accumulate(const uint8_t *img, const ImgLayout &lay, const es_traces &tr,
                                     const es_replay_out &out, uint32_t n_groups, uint64_t *counts,
                                     uint64_t *hist0, cudaStream_t st);

@@ -35,26 +35,28 @@ def _all_reduce(x, group):
     dist.all_reduce(x.view(torch.int64), op=dist.ReduceOp.SUM, group=group)
 
 
-def group_merge(prof, dtr, out, n_groups, group=None, stream=None):
+def group_merge(prof, dtr, out, n_groups, group=None, stream=None, with_p95=False):
     """Exact per-group counters and nearest-rank P95 across all ranks.
 
     dtr: uploaded traces of this rank's scenarios; out: this rank's replay
     outputs.  group: a torch.distributed process group (None = default when
-    initialised, False = local only).  Returns (counts u64 [G][7], p95 u64 [G]).
+    initialised, False = local only).  with_p95: also compute the per-scenario
+    P95 (K3) in the same pass as the level-0 histogram.  Returns
+    (counts u64 [G][7], p95 u64 [G]).
     """
     import torch
-    from . import ES_HIST_BINS, ES_NGSTAT, es_group_accumulate, es_group_hist, es_group_p95_select
+    from . import ES_HIST_BINS, ES_NGSTAT, es_group_hist, es_group_p95_select, es_scen_stats
     dev = dtr["arrival"].device
     G = int(n_groups)
     buf = torch.zeros(G * ES_NGSTAT + G * ES_HIST_BINS, dtype=torch.uint64, device=dev)
     counts = buf[:G * ES_NGSTAT]
     hist = buf[G * ES_NGSTAT:]
     state = torch.zeros(2 * G, dtype=torch.uint64, device=dev)
-    es_group_accumulate(prof, dtr["arr_off"], dtr["arrival"], out, G, counts, hist, dtr["cfg_idx"],
-                        dtr["group_id"], stream)
+    es_scen_stats(prof, dtr["arr_off"], dtr["arrival"], out, G, counts, hist, dtr["cfg_idx"], dtr["group_id"],
+                  p95=with_p95, stream=stream)
     _all_reduce(buf, group)
     es_group_p95_select(G, 0, counts, hist, state, stream)
-    for level in (1, 2):
+    for level in (1, 2, 3):
         es_group_hist(prof, dtr["arr_off"], dtr["arrival"], out, G, level, state, hist, dtr["cfg_idx"],
                       dtr["group_id"], stream)
         _all_reduce(hist, group)
@@ -66,8 +68,8 @@ def replay_group_stats(prof, dtr, n_groups, full=False, group=None, stream=None,
     """One pass of the whole hot path: K2 replay + K3 P95 + group merge."""
     from . import es_replay_traces
     out = es_replay_traces(prof, dtr["arr_off"], dtr["arrival"], dtr["cfg_idx"], dtr["group_id"], out=out,
-                           full=full, stream=stream)
-    counts, p95 = group_merge(prof, dtr, out, n_groups, group=group, stream=stream)
+                           full=full, p95=False, stream=stream)
+    counts, p95 = group_merge(prof, dtr, out, n_groups, group=group, stream=stream, with_p95=True)
     return out, counts, p95
 
 
@@ -85,4 +87,5 @@ def weak_ids(per_rank, rank):
     return np.arange(rank * per_rank, (rank + 1) * per_rank, dtype=np.int64)
 
 
-RADIX_LEVELS = ((20, 12), (8, 12), (0, 8))  # (shift, bits) of the 3 group-P95 selection levels
+# group-P95 radix levels (normal path): level 0 coarse min(T >> 12, 4095), level 1 T & 0xFFF
+COARSE_SHIFT, COARSE_OVF = 12, 4095

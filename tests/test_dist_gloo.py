@@ -1,6 +1,7 @@
 """Multi-rank plumbing on CPU (gloo, world_size 2): scenario sharding, the int64
 all_reduce of u64 counters/histograms used between radix levels, and the exactness
-of the 3-level group-P95 protocol (levels of engine.RADIX_LEVELS) after summing
+of the group-P95 radix protocol of include/edgeserve.h (coarse min(T >> 12, 4095),
+then T & 0xFFF, or T >> 20 / (T >> 8) & 0xFFF / T & 0xFF in overflow) after summing
 per-rank histograms -- checked against the oracle's P95 of the union."""
 import math
 import os
@@ -25,15 +26,24 @@ def _free_port():
     return p
 
 
-def _hist_level(lat, level, prefix):
-    shift, bits = engine.RADIX_LEVELS[level]
-    h = np.zeros(4096, np.uint64)
+def _digit(lat, level, ovf, prefix):
+    """(take mask, bin) of one radix level, as documented in include/edgeserve.h."""
     if level == 0:
-        sel = lat
-    else:
-        pshift = engine.RADIX_LEVELS[level - 1][0]
-        sel = lat[(lat >> pshift) == prefix]
-    np.add.at(h, ((sel >> shift) & ((1 << bits) - 1)).astype(np.int64), 1)
+        return np.ones(lat.size, bool), np.minimum(lat >> 12, 4095)
+    if not ovf:
+        return (lat >> 12) == prefix, lat & 0xFFF
+    big = (lat >> 12) >= 4095
+    if level == 1:
+        return big, lat >> 20
+    if level == 2:
+        return big & ((lat >> 20) == prefix), (lat >> 8) & 0xFFF
+    return big & ((lat >> 8) == prefix), lat & 0xFF
+
+
+def _hist_level(lat, level, ovf, prefix):
+    take, b = _digit(lat, level, ovf, prefix)
+    h = np.zeros(4096, np.uint64)
+    np.add.at(h, b[take].astype(np.int64), 1)
     return h
 
 
@@ -66,13 +76,25 @@ def _worker(rank, world, port, n_scen, q):
     for g in range(G):
         N = int(counts[g, 0])
         k = (95 * N + 99) // 100
-        prefix = 0
-        for level in range(3):
-            h = torch.from_numpy(_hist_level(lats[g], level, prefix).astype(np.int64))
+        prefix, ovf = 0, False
+        for level in range(4):
+            h = torch.from_numpy(_hist_level(lats[g], level, ovf, prefix).astype(np.int64))
             engine._all_reduce(h, None)
+            if N == 0:
+                continue
             b, k = _select(h.numpy(), k)
-            prefix = b if level == 0 else (prefix << engine.RADIX_LEVELS[level][1]) | b
-        result.append(prefix)
+            if level == 0:
+                prefix, ovf = b, b == 4095
+            elif not ovf:
+                prefix = (prefix << 12) | b
+                break
+            elif level == 1:
+                prefix = b
+            elif level == 2:
+                prefix = (prefix << 12) | b
+            else:
+                prefix = (prefix << 8) | b
+        result.append(prefix if N else 0)
     q.put((rank, ids.tolist(), counts.tolist(), result))
     dist.barrier()
     dist.destroy_process_group()

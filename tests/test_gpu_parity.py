@@ -325,3 +325,23 @@ def test_group_merge_rank_count_invariance():
     for c, p in results:
         assert np.array_equal(c, oc)
         assert np.array_equal(p.astype(np.uint32), op)
+
+
+def test_group_merge_overflow_bin():
+    """Group P95 beyond 16.77 s (the coarse overflow bin): the 4-level path."""
+    prof = inputs.Profile(M=1, E=1, bs=np.array([1], np.int32), lat=np.array([[[12000]]], np.uint32),
+                          mask=np.ones((1, 1), np.uint8))
+    cfgs = [inputs.SchedCfg(tau=50000, b_max=1, warmup=5)]
+    scen = [[[0] * 1900], [list(range(0, 3000000, 7000))], [[10] * 1500 + [20000000] * 30]]
+    segs = [[np.asarray(q, np.uint32) for q in sc] for sc in scen]
+    tr = inputs._assemble(1, segs, [0, 0, 0], [0, 1, 0], np.arange(3))
+    w = inputs.Workload("ovf", prof, cfgs, tr, 0)
+    g = run_k2(w)
+    counts, p95 = es.group_merge(g["_handle"], g["_dev"], g["_out"], 2, group=False, with_p95=False)
+    torch.cuda.synchronize()
+    o = oracle.replay_batch(prof, cfgs, tr)
+    oc, op = oracle.group_stats(tr, o, cfgs, 2)
+    assert int(op[0]) > (4095 << 12)  # really in the overflow bin
+    assert np.array_equal(np_of(counts), oc)
+    assert np.array_equal(np_of(p95).astype(np.uint32), op)
+    assert np.array_equal(g["p95"], o["p95"])
