@@ -11,6 +11,7 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -281,10 +282,19 @@ es_status es_replay_traces(const es_profile *p, const es_traces *tr, es_replay_o
   if (out->dec_cap < 0) return fail(ES_ERR_ARG, "dec_cap < 0");
   DeviceGuard guard(p->device);
   es_profile *pm = const_cast<es_profile *>(p);
-  int nl = 0;
-  CK(launch_replay(p->d_img, p->lay, *tr, *out, p->d_status, p->d_work, (cudaStream_t)stream, p->sms, &nl),
-     "k2_replay");
-  pm->launches += nl;
+  // K2 mapping: lane segments per scenario (k2_replay.cu, default) or
+  // ES_K2=lane: one lane per model queue (k2_lane.cu; same integers)
+  const char *k2 = getenv("ES_K2");
+  if (!(k2 && strcmp(k2, "lane") == 0)) {
+    int nl = 0;
+    CK(launch_replay(p->d_img, p->lay, *tr, *out, p->d_status, p->d_work, (cudaStream_t)stream, p->sms, &nl),
+       "k2_replay");
+    pm->launches += nl;
+  } else {
+    CK(launch_replay_lane(p->d_img, p->lay, *tr, *out, p->d_status, p->d_work, (cudaStream_t)stream, p->sms),
+       "k2_lane");
+    pm->launches++;
+  }
   if (out->scen_p95_us) {
     CK(launch_scen_p95(p->d_img, p->lay, *tr, *out, (cudaStream_t)stream, p->sms), "k3_scen_p95");
     pm->launches++;

@@ -345,3 +345,15 @@ def test_group_merge_overflow_bin():
     assert np.array_equal(np_of(counts), oc)
     assert np.array_equal(np_of(p95).astype(np.uint32), op)
     assert np.array_equal(g["p95"], o["p95"])
+
+
+def test_k2_lane_mapping_matches_oracle(monkeypatch):
+    """The alternative one-lane-per-model K2 mapping (ES_K2=lane) gives the
+    same bits as the oracle on cfg2/cfg3 subsets and the edge cases."""
+    monkeypatch.setenv("ES_K2", "lane")
+    for name, ids, n_req in [("cfg2", list(range(0, 60, 3)), 1500), ("cfg3", list(range(0, 54, 3)), 1200)]:
+        w = inputs.workload(name, scen_ids=ids, n_req=n_req)
+        g = run_k2(w, dec_cap=2000)
+        o = oracle.replay_batch(w.profile, w.cfgs, w.traces, dec_cap=2000, nthreads=8)
+        assert_k2_equal(g, o, 2000)
+    test_k2_edge_cases()
