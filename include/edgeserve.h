@@ -128,6 +128,9 @@ typedef struct {
   const uint64_t *q_off;    /* [n*M+1] CSR: queue (s,m) = waits[q_off[s*M+m] ..
                                q_off[s*M+m+1])                                      */
   const uint32_t *waits_us; /* head (oldest) first, non-increasing per queue (Q7)  */
+  int64_t n_waits;          /* q_off[n*M] if known (host value), else 0.  Selects the
+                               mapping: >= 1024 waits per snapshot on average -> one
+                               CTA per snapshot (deep queues), else a warp segment     */
 } es_snapshots;
 
 #define ES_FLAG_FEASIBLE 1u  /* Eq. 6 satisfiable for the chosen model            */

@@ -47,7 +47,7 @@ class SchedCfg(ctypes.Structure):
 
 
 class Snapshots(ctypes.Structure):
-    _fields_ = [("n", ctypes.c_int64), ("cfg_idx", P), ("q_off", P), ("waits_us", P)]
+    _fields_ = [("n", ctypes.c_int64), ("cfg_idx", P), ("q_off", P), ("waits_us", P), ("n_waits", ctypes.c_int64)]
 
 
 class Decisions(ctypes.Structure):
@@ -197,7 +197,7 @@ def es_score_candidates(prof: Profile, q_off, waits, cfg_idx=None, cand=True, ou
                "B": torch.empty(n, dtype=torch.uint16, device=dev), "L": torch.empty(n, dtype=torch.uint32, device=dev),
                "S": torch.empty(n, dtype=torch.uint64, device=dev), "flags": torch.empty(n, dtype=torch.uint8, device=dev),
                "cand": torch.empty(n * prof.M, dtype=torch.uint64, device=dev) if cand else None}
-    sn = Snapshots(n, _ptr(cfg_idx), _ptr(q_off), _ptr(waits))
+    sn = Snapshots(n, _ptr(cfg_idx), _ptr(q_off), _ptr(waits), int(waits.numel()))
     dc = Decisions(_ptr(out["m"]), _ptr(out["e"]), _ptr(out["B"]), _ptr(out["L"]), _ptr(out["S"]),
                    _ptr(out["flags"]), _ptr(out.get("cand")))
     _check(lib().es_score_candidates(prof.handle, ctypes.byref(sn), ctypes.byref(dc), _stream(stream)))

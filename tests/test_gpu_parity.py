@@ -357,3 +357,16 @@ def test_k2_lane_mapping_matches_oracle(monkeypatch):
         o = oracle.replay_batch(w.profile, w.cfgs, w.traces, dec_cap=2000, nthreads=8)
         assert_k2_equal(g, o, 2000)
     test_k2_edge_cases()
+
+
+@pytest.mark.parametrize("mode", ["block", "seg"])
+def test_k1_both_mappings(monkeypatch, mode):
+    """K1's two mappings (one CTA per snapshot for deep queues, warp segments
+    for small ones) on every K1 input family."""
+    monkeypatch.setenv("ES_K1", mode)
+    test_k1_random_states(3)
+    test_k1_random_states(8)
+    test_k1_deep_snapshots(8, 4096)
+    test_k1_deep_snapshots(4, 300)
+    test_k1_masks_and_flags()
+    test_k1_harvested_snapshots()
