@@ -198,6 +198,13 @@ es_status es_load_profile(const es_profile_desc *desc, const es_sched_cfg *cfgs,
   }
   memcpy(img.data() + lay.off_cfg, recs.data(), sizeof(CfgRec) * ncfg);
 
+  {  // keep stream-ordered scratch (K1 streaming phases) cached in the pool
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+      uint64_t thr = UINT64_MAX;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+  }
   es_profile *p = new es_profile();
   p->device = device;
   p->lay = lay;

@@ -49,6 +49,8 @@ struct DevStatus {
 cudaError_t launch_build_tables(uint8_t *img, const ImgLayout &lay, cudaStream_t st);
 cudaError_t launch_score(const uint8_t *img, const ImgLayout &lay, const es_snapshots &sn,
                          const es_decisions &out, DevStatus *dstat, cudaStream_t st, int sms);
+cudaError_t launch_score_stream(const uint8_t *img, const ImgLayout &lay, const es_snapshots &sn,
+                                const es_decisions &out, DevStatus *dstat, cudaStream_t st, int sms);
 cudaError_t launch_replay(const uint8_t *img, const ImgLayout &lay, const es_traces &tr,
                           const es_replay_out &out, DevStatus *dstat, uint32_t *work_ctr,
                           cudaStream_t st, int sms, int *n_launch);

@@ -421,9 +421,9 @@ cudaError_t launch_score(const uint8_t *img, const ImgLayout &lay, const es_snap
   a.dstat = dstat;
   // deep snapshots (>= 1024 waits each on average): one CTA per snapshot
   const char *k1 = getenv("ES_K1");
-  const bool block = k1 ? strcmp(k1, "block") == 0
-                        : (sn.n_waits > 0 && sn.n > 0 && sn.n_waits / sn.n >= 1024);
-  if (block) {
+  const bool deep = sn.n_waits > 0 && sn.n > 0 && sn.n_waits / sn.n >= 1024;
+  if (k1 ? strcmp(k1, "stream") == 0 : deep) return launch_score_stream(img, lay, sn, out, dstat, st, sms);
+  if (k1 && strcmp(k1, "block") == 0) {
     if (lay.M <= 2) return launch_block<2>(img, lay, a, st, sms);
     if (lay.M <= 4) return launch_block<4>(img, lay, a, st, sms);
     return launch_block<8>(img, lay, a, st, sms);

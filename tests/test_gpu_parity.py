@@ -359,10 +359,10 @@ def test_k2_lane_mapping_matches_oracle(monkeypatch):
     test_k2_edge_cases()
 
 
-@pytest.mark.parametrize("mode", ["block", "seg"])
-def test_k1_both_mappings(monkeypatch, mode):
-    """K1's two mappings (one CTA per snapshot for deep queues, warp segments
-    for small ones) on every K1 input family."""
+@pytest.mark.parametrize("mode", ["stream", "block", "seg"])
+def test_k1_all_mappings(monkeypatch, mode):
+    """K1's mappings (3-phase streaming and one CTA per snapshot for deep
+    queues, warp segments for small ones) on every K1 input family."""
     monkeypatch.setenv("ES_K1", mode)
     test_k1_random_states(3)
     test_k1_random_states(8)
