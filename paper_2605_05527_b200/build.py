@@ -27,16 +27,19 @@ def _stale(out, deps):
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(force=False, verbose=False, ptxas_v=False):
+def build(force=False, verbose=False, ptxas_v=False, lib=None, defines=()):
+    """Compile every csrc/*.cu and link the shared library (`lib`, default the
+    in-tree libedgeserve.so).  `defines` are extra -D flags (tuning variants)."""
+    lib = lib or LIB
     deps = sources() + glob.glob(os.path.join(CSRC, "*.cuh")) + [os.path.join(ROOT, "include", "edgeserve.h")]
-    if not force and not _stale(LIB, deps):
-        return LIB
-    objdir = os.path.join(HERE, "build")
+    if not force and not _stale(lib, deps):
+        return lib
+    objdir = os.path.join(HERE, "build" if lib == LIB else "build_" + os.path.basename(lib)[:-3])
     os.makedirs(objdir, exist_ok=True)
     objs = []
     for src in sources():
         obj = os.path.join(objdir, os.path.basename(src)[:-3] + ".o")
-        cmd = [NVCC, *ARCH, *FLAGS, "-c", src, "-o", obj]
+        cmd = [NVCC, *ARCH, *FLAGS, *["-D" + d for d in defines], "-c", src, "-o", obj]
         if ptxas_v:
             cmd += ["-Xptxas", "-v"]
         if verbose:
@@ -44,10 +47,14 @@ def build(force=False, verbose=False, ptxas_v=False):
         subprocess.check_call(cmd)
         objs.append(obj)
     # exported symbols: the es_* C ABI (api.cu marks them default visibility)
-    cmd = [NVCC, *ARCH, "-shared", "-o", LIB, *objs, "-Xcompiler", "-fPIC"]
+    cmd = [NVCC, *ARCH, "-shared", "-o", lib, *objs, "-Xcompiler", "-fPIC"]
     subprocess.check_call(cmd)
-    return LIB
+    return lib
 
 
 if __name__ == "__main__":
-    build(force="--force" in sys.argv, verbose=True, ptxas_v="-v" in sys.argv)
+    # python build.py [--force] [-v] [--lib PATH -DNAME=V ...]
+    args = sys.argv[1:]
+    lib = args[args.index("--lib") + 1] if "--lib" in args else None
+    defs = [x[2:] for x in args if x.startswith("-D")]
+    build(force="--force" in args, verbose=True, ptxas_v="-v" in args, lib=lib, defines=defs)

@@ -340,6 +340,11 @@ __device__ __forceinline__ Decision finish_decision(const Seg<LPS, MM> &sg, cons
   return d;
 }
 
+#ifndef ES_WU
+#define ES_WU 4
+#endif
+constexpr int WU = ES_WU;  // positions per lane per step in the G loops
+
 template <int LPS, int MM, class WaitAt>
 __device__ __forceinline__ Decision decide_general(const Seg<LPS, MM> &sg, const SmemProf &P, const SmemCfg &C,
                                                 uint32_t len, uint32_t c, const Cand &cand, uint32_t Bown,
@@ -368,13 +373,20 @@ __device__ __forceinline__ Decision decide_general(const Seg<LPS, MM> &sg, const
       else U[m] += gw;
     }
   }
-  for (; p < len; p += GL) {
-    const uint32_t w = wait_at(p);
-    const uint32_t gw = G_of(P, C, w);
+  for (; p < len; p += WU * GL) {
+    uint32_t w[WU];
 #pragma unroll
-    for (int m = 0; m < MM; ++m) {
-      if (w >= thr[m]) K[m] += 1u;
-      else U[m] += gw;
+    for (int k = 0; k < WU; ++k) w[k] = p + k * GL < len ? wait_at(p + k * GL) : 0u;
+#pragma unroll
+    for (int k = 0; k < WU; ++k) {
+      if (p + k * GL < len) {
+        const uint32_t gw = G_of(P, C, w[k]);
+#pragma unroll
+        for (int m = 0; m < MM; ++m) {
+          if (w[k] >= thr[m]) K[m] += 1u;
+          else U[m] += gw;
+        }
+      }
     }
   }
   __syncwarp();
@@ -425,10 +437,24 @@ __device__ __forceinline__ Decision decide(const Seg<LPS, MM> &sg, const SmemPro
   // per-candidate clip tests and 3 M reductions collapse to 4 reductions.
   if (!__any_sync(FULL, len > 0u && wmax >= C.fast_lim)) {
     uint64_t tot = 0ull, srv = 0ull;
-    for (uint32_t p = sg.gl; p < len; p += GL) {
-      const uint64_t gw = G_of(P, C, wait_at(p));
-      tot += gw;
-      if (p < Bown) srv += gw;
+    // WU positions per lane per step: their loads issue back to back (the
+    // per-decision chain is latency-bound, one queue is a handful of steps)
+    for (uint32_t p0 = sg.gl; p0 < len; p0 += WU * GL) {
+      uint32_t w[WU];
+#pragma unroll
+      for (int k = 0; k < WU; ++k) {
+        const uint32_t p = p0 + k * GL;
+        w[k] = p < len ? wait_at(p) : 0u;
+      }
+#pragma unroll
+      for (int k = 0; k < WU; ++k) {
+        const uint32_t p = p0 + k * GL;
+        if (p < len) {
+          const uint64_t gw = G_of(P, C, w[k]);
+          tot += gw;
+          if (p < Bown) srv += gw;
+        }
+      }
     }
     __syncwarp();
     tot = sg.sum64(tot);

@@ -55,9 +55,17 @@ struct ReplayArgs {
 
 __device__ __forceinline__ uint32_t ldg_u32(const uint32_t *p) { return __ldg(p); }
 
+// L1 prefetch of an upcoming arrival line (admission reads it a few decisions later)
+__device__ __forceinline__ void prefetch_l1(const uint32_t *p) { asm volatile("prefetch.global.L1 [%0];" ::"l"(p)); }
+
 __device__ __forceinline__ void report(DevStatus *ds, uint32_t code, int64_t item) {
   if (atomicCAS(&ds->code, 0u, code) == 0u) ds->item = (unsigned long long)item;
 }
+
+#ifndef ES_PF_LINES
+#define ES_PF_LINES 2
+#endif
+constexpr int PF_LINES = ES_PF_LINES;
 
 template <int LPS, int MM>
 __global__ void __launch_bounds__(256) k2_replay(const uint8_t *__restrict__ gimg, ImgLayout lay, ReplayArgs a) {
@@ -160,6 +168,12 @@ __global__ void __launch_bounds__(256) k2_replay(const uint8_t *__restrict__ gim
           if (sg.sbits(badb)) status = ES_ERR_UNSORTED;
         }
         more = __any_sync(FULL, run && status == ES_OK && cnt == (uint32_t)GL);
+      }
+      // keep the next PF_LINES 128-byte lines of this model's arrivals in L1
+      // (the admission loads above are the head of the per-decision chain)
+      if (run && sg.gl < PF_LINES) {
+        const uint32_t pf = (tail & ~31u) + 32u * (uint32_t)(sg.gl + 1);
+        if (pf < n) prefetch_l1(Aq + pf);
       }
       const bool go = run && status == ES_OK;
       uint32_t len = go ? tail - head : 0u;
