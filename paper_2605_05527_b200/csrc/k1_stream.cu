@@ -32,6 +32,10 @@ struct QRec {  // per (snapshot, model) queue
 
 constexpr int ACC = 2 + 2 * MAXM;  // tot, flags, S-part[8] (srv or U), K[8]
 constexpr uint64_t F_SLOW = 1, F_BAD = 2;
+#ifndef ES_K1_MINB
+#define ES_K1_MINB 4
+#endif
+constexpr uint32_t V4_LIM = (1u << 30) - 1024u;  // fast-stream G needs 4 (x_c + 1023) < 2^32
 
 struct StreamArgs {
   int64_t n;
@@ -96,7 +100,7 @@ __global__ void __launch_bounds__(256) k1s_prep(const uint8_t *__restrict__ gimg
       r.ef = e | (best >= 0 ? 0x80u : 0u);
       r.thr = r.L < C.x_c ? C.x_c - r.L : 0u;
       r.H = r.L < C.x_c ? reinterpret_cast<const uint64_t *>(P.sm + C.off_H)[((size_t)g * P.E + e) * P.nb + bi] : 0ull;
-      if (wmax >= C.fast_lim) {
+      if (wmax >= C.fast_lim || C.x_c > V4_LIM) {
         const unsigned long long was = atomicOr(a.acc + s * ACC + 1, F_SLOW);
         if (!(was & F_SLOW)) a.slow_list[atomicAdd(a.slow_n, 1ull)] = s;
       }
@@ -119,110 +123,104 @@ __device__ __forceinline__ uint32_t lds_u32(uint32_t saddr) {
 }
 
 // G(w) for a live wait (w < x_c guaranteed by the prefix search; an inverted
-// input is flagged and its value unused, the index is clamped for safety)
+// input is flagged and its value unused, the index is clamped for safety).
+// v4 = 4 (w + r) in one IMAD: exact while x_c + 1024 <= 2^30 (k1s_prep routes
+// other SLOs to the clip path, which uses the plain form).
 struct GTab {
-  uint32_t sA, sBt, r, nA1;
+  uint32_t sA, sBt, r4, nA1;
   __device__ __forceinline__ uint32_t operator()(uint32_t w) const {
-    const uint32_t v = w + r;
-    const uint32_t h = min(v >> SBITS, nA1);
+    const uint32_t v4 = w * 4u + r4;
+    const uint32_t h = min(v4 >> (SBITS + 2), nA1);
     const uint32_t a = lds_u32(sA + 4u * h);
-    const uint32_t b = lds_u32(sBt + 4u * (v & (S - 1u)));
+    const uint32_t b = lds_u32(sBt + (v4 & (4u * S - 4u)));
     return (uint32_t)(((uint64_t)a * (uint64_t)b) >> F);
   }
 };
 
-// ---------------------------------------------------------------------------
-// Fast path (snapshot cannot clip): sum of G over every live window.
-//
-// The flat waits array [q_off[0], q_off[nq]) is cut into equal contiguous
-// ranges, one per warp (balanced in bytes whatever the queue-length mix).  A
-// warp finds its first queue with a 32-ary search over q_off and walks the
-// queues ("pieces") intersecting its range.  The 16-byte aligned body of each
-// piece streams through a per-warp ring of NST shared-memory stages filled by
-// TMA bulk copies (cp.async.bulk, one per 2 KB chunk, completing on a
-// per-stage mbarrier); the producer runs NST chunks ahead across piece
-// boundaries, so HBM traffic stays in flight while the warp evaluates G.
-// The unaligned head/tail (<= 3 + 3 waits) and the candidate's own served
-// head (positions < B) are read directly when a piece is opened.
-// Read-window validation (Q24): every wait is compared with its predecessor.
-#ifndef ES_K1_NST
-#define ES_K1_NST 3
-#endif
-constexpr int NST = ES_K1_NST;    // stages per warp
-constexpr uint32_t CHW = 512;     // waits per chunk (2 KB)
-constexpr int FAST_WARPS = 8;     // 256 threads
+__device__ __forceinline__ void load_stage(const uint4 *__restrict__ V, uint32_t nv, uint32_t v0, int lane, uint4 &c0,
+                                           uint4 &c1) {
+  const uint4 z = make_uint4(0u, 0u, 0u, 0u);
+  c0 = v0 + lane < nv ? __ldg(V + v0 + lane) : z;
+  c1 = v0 + 32u + lane < nv ? __ldg(V + v0 + 32u + lane) : z;
+}
 
-struct ChunkDesc {  // written by lane 0 when the chunk is issued
-  int64_t s;        // snapshot (accumulator row)
-  uint32_t n;       // waits in the chunk (multiple of 4)
-  uint32_t flags;   // CH_FIRST / CH_LAST chunk of its piece (LAST: flush the piece total)
-  uint32_t carry;   // first chunk: wait preceding it (0xFFFFFFFF: none)
-  uint32_t sA, sBt, r, nA1;
-};
-static_assert(sizeof(ChunkDesc) == 40, "ChunkDesc");
-constexpr uint32_t CH_FIRST = 1, CH_LAST = 2;
-
-struct WarpRing {
-  uint8_t buf[NST][CHW * 4];
-  ChunkDesc desc[NST];
-  uint64_t bar[NST];
-};
-constexpr size_t FAST_RING_BYTES = sizeof(WarpRing) * FAST_WARPS;
-
-__device__ __forceinline__ void mbar_wait(uint32_t mb, uint32_t parity) {
-  uint32_t done = 0;
-  while (!done) {
-    asm volatile(
-        "{\n\t.reg .pred p;\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
-        "selp.u32 %0, 1, 0, p;\n\t}"
-        : "=r"(done)
-        : "r"(mb), "r"(parity)
-        : "memory");
+// vectors [v0, v0 + 64): lane holds v0 + lane (c0) and v0 + 32 + lane (c1);
+// `carry` = last wait before v0 (0xFFFFFFFF: none)
+__device__ __forceinline__ void sum_stage(const GTab &G, uint32_t nv, uint32_t v0, int lane, const uint4 &c0,
+                                          const uint4 &c1, uint32_t &carry, uint64_t &tot, bool &bad) {
+#pragma unroll
+  for (int k = 0; k < 2; ++k) {
+    const uint4 cur = k ? c1 : c0;
+    uint32_t prev = __shfl_up_sync(FULL, cur.w, 1);
+    if (lane == 0) prev = carry;
+    carry = __shfl_sync(FULL, cur.w, 31);
+    if (v0 + 32u * k + lane < nv) {
+      bad |= (cur.x > prev) | (cur.y > cur.x) | (cur.z > cur.y) | (cur.w > cur.z);
+      tot += (uint64_t)G(cur.x) + G(cur.y) + (uint64_t)G(cur.z) + G(cur.w);
+    }
   }
 }
 
-__device__ __forceinline__ uint4 lds_u128(uint32_t saddr) {
-  uint4 v;
-  asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(saddr));
-  return v;
+// Sum of G over waits [ps, pe) of one queue (absolute positions in the waits
+// array), with the read-window neighbour check (Q24).  16-byte vector loads
+// (4 waits per lane, two vectors per lane per stage, next stage prefetched);
+// scalar head up to 16-byte alignment and scalar tail; one shuffle per vector
+// carries the predecessor across lanes.  `first` = position of the queue's
+// first live wait (no predecessor check there).
+__device__ __forceinline__ void stream_piece(const uint32_t *__restrict__ W, uint64_t ps, uint64_t pe, uint64_t first,
+                                             const GTab &G, int lane, uint64_t &tot, bool &bad) {
+  const uint32_t mis = (uint32_t)(((uintptr_t)(W + ps) >> 2) & 3u);
+  const uint64_t pa = min(ps + (uint64_t)((4u - mis) & 3u), pe);
+  const uint32_t nv = (uint32_t)((pe - pa) / 4u);
+  const uint64_t pt = pa + 4ull * nv;
+  {
+    const uint32_t nh = (uint32_t)(pa - ps), ntl = (uint32_t)(pe - pt);
+    uint64_t p = ~0ull;
+    if (lane < (int)nh) p = ps + lane;
+    else if (lane >= 8 && lane < 8 + (int)ntl) p = pt + (lane - 8);
+    if (p != ~0ull) {
+      const uint32_t w = __ldg(W + p);
+      if (p > first && w > __ldg(W + p - 1)) bad = true;
+      tot += G(w);
+    }
+  }
+  const uint4 *V = reinterpret_cast<const uint4 *>(W + pa);
+  uint32_t carry = pa > first ? __ldg(W + pa - 1) : 0xFFFFFFFFu;
+  // stage X = vectors [v0, v0 + 64), stage Y = [v0 + 64, v0 + 128): two
+  // vectors per lane each; one stage is in flight while the other is summed
+  uint4 x0, x1, y0, y1;
+  load_stage(V, nv, 0u, lane, x0, x1);
+  for (uint32_t v0 = 0; v0 < nv; v0 += 128u) {  // warp-uniform trip count
+    load_stage(V, nv, v0 + 64u, lane, y0, y1);
+    sum_stage(G, nv, v0, lane, x0, x1, carry, tot, bad);
+    if (v0 + 64u >= nv) break;
+    load_stage(V, nv, v0 + 128u, lane, x0, x1);
+    sum_stage(G, nv, v0 + 64u, lane, y0, y1, carry, tot, bad);
+  }
 }
 
-// warp-uniform producer state: the piece being copied and the next position
-struct Producer {
-  int64_t q;          // queue of the current piece
-  uint64_t pos, pt;   // next position to copy, end of the aligned body
-  int64_t s;
-  uint32_t carry;     // predecessor of the piece's first chunk
-  bool first;         // next chunk is the piece's first
-  GTab G;
-  bool done;
-};
-
-__global__ void __launch_bounds__(256, 3) k1s_stream_fast(const uint8_t *__restrict__ gimg, ImgLayout lay,
-                                                       StreamArgs a) {
+// fast path (snapshot cannot clip): sum of G over every live window.  The
+// flat waits array [q_off[0], q_off[nq]) is cut into equal contiguous ranges,
+// one per warp (balanced in bytes whatever the queue-length mix); a warp finds
+// its first queue with a 32-ary search over q_off, then walks the queues that
+// intersect its range.  Per piece: u64 atomics into the snapshot's total and
+// into the candidate's own served-head sum (positions < B).
+__global__ void __launch_bounds__(256, ES_K1_MINB) k1s_stream_fast(const uint8_t *__restrict__ gimg, ImgLayout lay,
+                                                         StreamArgs a) {
   extern __shared__ __align__(16) uint8_t smem[];
   __shared__ uint64_t mbar;
   stage_image(smem, gimg, lay.bytes, &mbar);
   const SmemProf P = smem_prof(smem, lay);
   const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(smem);
   const int M = P.M;
-  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-  WarpRing &R = reinterpret_cast<WarpRing *>(smem + ((lay.bytes + 127u) & ~127u))[wib];
-  const uint32_t sbuf = (uint32_t)__cvta_generic_to_shared(&R.buf[0][0]);
-  const uint32_t sbar = (uint32_t)__cvta_generic_to_shared(&R.bar[0]);
-  if (lane == 0) {
-    for (int k = 0; k < NST; ++k) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(sbar + 8u * k));
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  __syncwarp();
+  const int lane = threadIdx.x & 31;
   const int64_t wid = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
   const int64_t nq = a.n * M;
   if (nq == 0) return;
   const uint64_t base = __ldg(a.q_off), end = __ldg(a.q_off + nq);
   uint64_t per = ((end - base) + (uint64_t)nw - 1u) / (uint64_t)nw;
-  per = max((per + 3u) & ~3ull, 1024ull);
+  per = max((per + 3u) & ~3ull, 512ull);
   const uint64_t x0 = base + (uint64_t)wid * per;
   if (x0 >= end) return;  // warp-uniform
   const uint64_t x1 = min(x0 + per, end);
@@ -235,140 +233,30 @@ __global__ void __launch_bounds__(256, 3) k1s_stream_fast(const uint8_t *__restr
     lo += step * l;
     hi = min(hi, lo + step);
   }
-  const uint32_t *W = a.waits;
-  Producer pr{};
-  pr.q = lo - 1;
-  pr.pos = pr.pt = 0;
-  pr.done = false;
-
-  // open the next piece: scalar head / tail / served head, immediate atomics;
-  // leaves pr.pos < pr.pt if the piece has an aligned body to stream
-  auto open_piece = [&]() {
-    for (;;) {  // warp-uniform
-      ++pr.q;
-      if (pr.q >= nq) {
-        pr.done = true;
-        return;
-      }
-      const QRec r = a.rec[pr.q];
-      if (r.lo >= x1) {
-        pr.done = true;
-        return;
-      }
-      if (r.len <= r.c) continue;
-      const uint64_t first = r.lo + r.c;
-      const uint64_t ps = max(first, x0), pe = min(r.lo + r.len, x1);
-      if (ps >= pe) continue;
-      const int64_t s = pr.q / M;
-      unsigned long long *acc = a.acc + s * ACC;
-      if ((*reinterpret_cast<volatile unsigned long long *>(acc + 1) & F_SLOW) != 0ull) continue;
-      const SmemCfg C = smem_cfg(P, a.cfg_idx ? (int)a.cfg_idx[s] : 0);
-      const GTab G{sbase + C.off_A, sbase + C.off_Bt, C.r, C.nA1};
-      // aligned body [pa, pt): 16-byte aligned addresses
-      const uint32_t mis = (uint32_t)(((uintptr_t)(W + ps) >> 2) & 3u);
-      const uint64_t pa = min(ps + (uint64_t)((4u - mis) & 3u), pe);
-      const uint64_t pt = pa + ((pe - pa) & ~3ull);
-      // scalar waits: head lanes 0..2 -> [ps, pa), tail lanes 8..10 -> [pt, pe)
-      uint64_t p = ~0ull;
-      if (lane < (int)(pa - ps)) p = ps + lane;
-      else if (lane >= 8 && lane < 8 + (int)(pe - pt)) p = pt + (lane - 8);
-      uint64_t tot = 0, srv = 0;
-      bool bad = false;
-      if (p != ~0ull) {
-        const uint32_t w = __ldg(W + p);
-        if (p > first && w > __ldg(W + p - 1)) bad = true;
-        tot += G(w);
-      }
-      const uint64_t se = min(pe, r.lo + min(r.B, r.len));
-      for (uint64_t q2 = ps + lane; q2 < se; q2 += 32u) srv += G(__ldg(W + q2));
-      if (__any_sync(FULL, bad) && lane == 0) atomicOr(acc + 1, F_BAD);
-      tot = wsum64(tot);
-      srv = wsum64(srv);
-      if (lane == 0) {
-        if (tot) atomicAdd(acc + 0, (unsigned long long)tot);
-        if (srv) atomicAdd(acc + 2 + (pr.q - s * M), (unsigned long long)srv);
-      }
-      if (pa >= pt) continue;  // no aligned body
-      pr.pos = pa;
-      pr.pt = pt;
-      pr.s = s;
-      pr.G = G;
-      pr.carry = pa > first ? __ldg(W + pa - 1) : 0xFFFFFFFFu;
-      pr.first = true;
-      return;
-    }
-  };
-  // issue the next chunk into stage k (returns false when the range is done)
-  auto produce = [&](int k) -> bool {
-    if (pr.pos >= pr.pt) open_piece();
-    if (pr.done) return false;
-    const uint32_t n = (uint32_t)min((uint64_t)CHW, pr.pt - pr.pos);
+  for (int64_t q = lo; q < nq; ++q) {  // warp-uniform
+    const QRec r = a.rec[q];
+    if (r.lo >= x1) break;
+    if (r.len <= r.c) continue;
+    const uint64_t first = r.lo + r.c;
+    const uint64_t ps = max(first, x0), pe = min(r.lo + r.len, x1);
+    if (ps >= pe) continue;
+    const int64_t s = q / M;
+    unsigned long long *acc = a.acc + s * ACC;
+    if ((*reinterpret_cast<volatile unsigned long long *>(acc + 1) & F_SLOW) != 0ull) continue;
+    const SmemCfg C = smem_cfg(P, a.cfg_idx ? (int)a.cfg_idx[s] : 0);
+    const GTab G{sbase + C.off_A, sbase + C.off_Bt, 4u * C.r, C.nA1};
+    uint64_t tot = 0, srv = 0;
+    bool bad = false;
+    stream_piece(a.waits, ps, pe, first, G, lane, tot, bad);
+    const uint64_t se = min(pe, r.lo + min(r.B, r.len));
+    for (uint64_t p = ps + lane; p < se; p += 32u) srv += G(__ldg(a.waits + p));
+    if (__any_sync(FULL, bad) && lane == 0) atomicOr(acc + 1, F_BAD);
+    tot = wsum64(tot);
+    srv = wsum64(srv);
     if (lane == 0) {
-      ChunkDesc &d = R.desc[k];
-      d.s = pr.s;
-      d.n = n;
-      d.flags = (pr.first ? CH_FIRST : 0u) | (pr.pos + n >= pr.pt ? CH_LAST : 0u);
-      d.carry = pr.carry;
-      d.sA = pr.G.sA;
-      d.sBt = pr.G.sBt;
-      d.r = pr.G.r;
-      d.nA1 = pr.G.nA1;
-      const uint32_t mb = sbar + 8u * k;
-      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(mb), "r"(n * 4u) : "memory");
-      asm volatile(
-          "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-              sbuf + (uint32_t)k * (CHW * 4u)),
-          "l"(W + pr.pos), "r"(n * 4u), "r"(mb)
-          : "memory");
+      atomicAdd(acc + 0, (unsigned long long)tot);
+      if (srv) atomicAdd(acc + 2 + (q - s * M), (unsigned long long)srv);
     }
-    pr.pos += n;
-    pr.first = false;
-    return true;
-  };
-
-  uint32_t issued = 0, consumed = 0;
-  while (issued < (uint32_t)NST && produce((int)issued)) ++issued;
-  uint64_t tot = 0;
-  uint32_t carry = 0xFFFFFFFFu;
-  bool bad = false;
-  while (consumed < issued) {  // warp-uniform
-    const int k = (int)(consumed % NST);
-    mbar_wait(sbar + 8u * k, (consumed / NST) & 1u);
-    const ChunkDesc d = R.desc[k];
-    const GTab G{d.sA, d.sBt, d.r, d.nA1};
-    if (d.flags & CH_FIRST) carry = d.carry;
-    const uint32_t nv = d.n / 4u;
-    const uint32_t sb = sbuf + (uint32_t)k * (CHW * 4u);
-    constexpr int VPL = (int)(CHW / 128u);  // vectors per lane per chunk
-    uint4 cv[VPL];
-#pragma unroll
-    for (int j = 0; j < VPL; ++j) {
-      const uint32_t v = 32u * j + lane;
-      cv[j] = v < nv ? lds_u128(sb + 16u * v) : make_uint4(0u, 0u, 0u, 0u);
-    }
-#pragma unroll
-    for (int j = 0; j < VPL; ++j) {
-      const uint4 cur = cv[j];
-      const uint32_t v = 32u * j + lane;
-      uint32_t prev = __shfl_up_sync(FULL, cur.w, 1);
-      if (lane == 0) prev = carry;
-      carry = __shfl_sync(FULL, cur.w, 31);
-      if (v < nv) {
-        bad |= (cur.x > prev) | (cur.y > cur.x) | (cur.z > cur.y) | (cur.w > cur.z);
-        tot += (uint64_t)G(cur.x) + G(cur.y) + (uint64_t)G(cur.z) + G(cur.w);
-      }
-    }
-    __syncwarp();  // every lane has read stage k before it is refilled
-    ++consumed;
-    if (d.flags & CH_LAST) {
-      unsigned long long *acc = a.acc + d.s * ACC;
-      if (__any_sync(FULL, bad) && lane == 0) atomicOr(acc + 1, F_BAD);
-      const uint64_t t = wsum64(tot);
-      if (lane == 0 && t) atomicAdd(acc + 0, (unsigned long long)t);
-      tot = 0;
-      bad = false;
-    }
-    if (produce(k)) ++issued;
   }
 }
 
@@ -564,9 +452,7 @@ cudaError_t launch_score_stream(const uint8_t *img, const ImgLayout &lay, const 
   a.rec = reinterpret_cast<QRec *>(sp + acc_bytes + list_bytes);
   e = cudaMemsetAsync(a.acc, 0, acc_bytes, st);
   if (e == cudaSuccess) e = launch_persistent(k1s_prep, img, lay, a, nq, 256, lay.bytes, st, sms);
-  if (e == cudaSuccess)
-    e = launch_persistent(k1s_stream_fast, img, lay, a, nq, 8, ((lay.bytes + 127u) & ~127u) + FAST_RING_BYTES, st,
-                          sms);
+  if (e == cudaSuccess) e = launch_persistent(k1s_stream_fast, img, lay, a, nq, 8, lay.bytes, st, sms);
   if (e == cudaSuccess) {
     if (lay.M <= 2) e = launch_persistent(k1s_stream_slow<2>, img, lay, a, nq, 8, lay.bytes, st, sms);
     else if (lay.M <= 4) e = launch_persistent(k1s_stream_slow<4>, img, lay, a, nq, 8, lay.bytes, st, sms);
