@@ -183,8 +183,8 @@ def bench_k1(es, h_cache, dev, stream, rank, n_snap=4096, depth=4096, iters=10):
                                                                              .sum().item()) / t_s,
             "ms_per_launch": t_s * 1e3, "feasible_frac": float((flags & 1).mean()),
             "roofline": {"bound": "hbm", "achieved": alg / t_s / 1e9, "peak": hbm, "unit": "GB/s",
-                         "frac": alg / t_s / 1e9 / hbm, "traffic": ncu_traffic("k1_score"),
-                         "kernel": "k1_score", "alg_bytes_per_launch": alg,
+                         "frac": alg / t_s / 1e9 / hbm, "traffic": ncu_traffic("k1_call"),
+                         "kernel": "k1 call: k1s_prep + k1s_stream_fast + k1s_stream_slow + k1s_finish", "alg_bytes_per_launch": alg,
                          "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({src})", "l2": "flushed between launches"}}
 
 

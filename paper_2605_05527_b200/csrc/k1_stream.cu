@@ -55,7 +55,12 @@ struct StreamArgs {
   int64_t *slow_list;          // their indices
 };
 
+// programmatic dependent launch (see launch_persistent)
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
 __global__ void __launch_bounds__(256) k1s_prep(const uint8_t *__restrict__ gimg, ImgLayout lay, StreamArgs a) {
+  pdl_trigger();
   extern __shared__ __align__(16) uint8_t smem[];
   __shared__ uint64_t mbar;
   stage_image(smem, gimg, lay.bytes, &mbar);
@@ -168,28 +173,34 @@ __device__ __forceinline__ void sum_stage(const GTab &G, uint32_t nv, uint32_t v
 // carries the predecessor across lanes.  `first` = position of the queue's
 // first live wait (no predecessor check there).
 __device__ __forceinline__ void stream_piece(const uint32_t *__restrict__ W, uint64_t ps, uint64_t pe, uint64_t first,
-                                             const GTab &G, int lane, uint64_t &tot, bool &bad) {
+                                             uint64_t se, const GTab &G, int lane, uint64_t &tot, uint64_t &srv,
+                                             bool &bad) {
   const uint32_t mis = (uint32_t)(((uintptr_t)(W + ps) >> 2) & 3u);
   const uint64_t pa = min(ps + (uint64_t)((4u - mis) & 3u), pe);
   const uint32_t nv = (uint32_t)((pe - pa) / 4u);
   const uint64_t pt = pa + 4ull * nv;
-  {
-    const uint32_t nh = (uint32_t)(pa - ps), ntl = (uint32_t)(pe - pt);
-    uint64_t p = ~0ull;
-    if (lane < (int)nh) p = ps + lane;
-    else if (lane >= 8 && lane < 8 + (int)ntl) p = pt + (lane - 8);
-    if (p != ~0ull) {
-      const uint32_t w = __ldg(W + p);
-      if (p > first && w > __ldg(W + p - 1)) bad = true;
-      tot += G(w);
-    }
-  }
   const uint4 *V = reinterpret_cast<const uint4 *>(W + pa);
-  uint32_t carry = pa > first ? __ldg(W + pa - 1) : 0xFFFFFFFFu;
-  // stage X = vectors [v0, v0 + 64), stage Y = [v0 + 64, v0 + 128): two
-  // vectors per lane each; one stage is in flight while the other is summed
+  // one round of loads: first stage, the body's predecessor, the scalar
+  // head/tail waits with theirs, the first 32 served-head waits
   uint4 x0, x1, y0, y1;
   load_stage(V, nv, 0u, lane, x0, x1);
+  uint32_t carry = pa > first ? __ldg(W + pa - 1) : 0xFFFFFFFFu;
+  const uint32_t nh = (uint32_t)(pa - ps), ntl = (uint32_t)(pe - pt);
+  uint64_t p = ~0ull;
+  if (lane < (int)nh) p = ps + lane;
+  else if (lane >= 8 && lane < 8 + (int)ntl) p = pt + (lane - 8);
+  const uint32_t sw = p != ~0ull ? __ldg(W + p) : 0u;
+  const uint32_t sp = (p != ~0ull && p > first) ? __ldg(W + p - 1) : 0xFFFFFFFFu;
+  const uint64_t p_srv = ps + lane;
+  const uint32_t ww = p_srv < se ? __ldg(W + p_srv) : 0u;
+  if (p != ~0ull) {
+    if (sw > sp) bad = true;
+    tot += G(sw);
+  }
+  if (p_srv < se) srv += G(ww);
+  for (uint64_t q2 = p_srv + 32u; q2 < se; q2 += 32u) srv += G(__ldg(W + q2));  // B > 32 only
+  // stage X = vectors [v0, v0 + 64), stage Y = [v0 + 64, v0 + 128): two
+  // vectors per lane each; one stage is in flight while the other is summed
   for (uint32_t v0 = 0; v0 < nv; v0 += 128u) {  // warp-uniform trip count
     load_stage(V, nv, v0 + 64u, lane, y0, y1);
     sum_stage(G, nv, v0, lane, x0, x1, carry, tot, bad);
@@ -207,6 +218,7 @@ __device__ __forceinline__ void stream_piece(const uint32_t *__restrict__ W, uin
 // into the candidate's own served-head sum (positions < B).
 __global__ void __launch_bounds__(256, ES_K1_MINB) k1s_stream_fast(const uint8_t *__restrict__ gimg, ImgLayout lay,
                                                          StreamArgs a) {
+  pdl_trigger();
   extern __shared__ __align__(16) uint8_t smem[];
   __shared__ uint64_t mbar;
   stage_image(smem, gimg, lay.bytes, &mbar);
@@ -233,23 +245,39 @@ __global__ void __launch_bounds__(256, ES_K1_MINB) k1s_stream_fast(const uint8_t
     lo += step * l;
     hi = min(hi, lo + step);
   }
+  // queue descriptors spread over the lanes (lane l < 10: word l of the QRec,
+  // lane 10: the snapshot's flag word, lane 11: its SLO index), fetched one
+  // piece ahead so the next piece's record is in flight while this one streams
+  static_assert(sizeof(QRec) == 40, "QRec");
+  auto fetch = [&](int64_t q) -> uint32_t {
+    if (q >= nq) return 0u;
+    const int64_t s = q / M;
+    if (lane < 10) return __ldg(reinterpret_cast<const uint32_t *>(a.rec + q) + lane);
+    if (lane == 10) return (uint32_t)a.acc[s * ACC + 1];  // F_SLOW is final (set by k1s_prep)
+    if (lane == 11) return a.cfg_idx ? (uint32_t)a.cfg_idx[s] : 0u;
+    return 0u;
+  };
+  pdl_wait();  // k1s_prep's records and flags
+  uint32_t dcur = fetch(lo);
   for (int64_t q = lo; q < nq; ++q) {  // warp-uniform
-    const QRec r = a.rec[q];
-    if (r.lo >= x1) break;
-    if (r.len <= r.c) continue;
-    const uint64_t first = r.lo + r.c;
-    const uint64_t ps = max(first, x0), pe = min(r.lo + r.len, x1);
+    const uint32_t dnext = fetch(q + 1);
+    const uint64_t rlo = (uint64_t)__shfl_sync(FULL, dcur, 0) | ((uint64_t)__shfl_sync(FULL, dcur, 1) << 32);
+    const uint32_t rlen = __shfl_sync(FULL, dcur, 4), rc = __shfl_sync(FULL, dcur, 5);
+    const uint32_t rB = __shfl_sync(FULL, dcur, 6);
+    const uint32_t flg = __shfl_sync(FULL, dcur, 10), k = __shfl_sync(FULL, dcur, 11);
+    dcur = dnext;
+    if (rlo >= x1) break;
+    if (rlen <= rc || (flg & (uint32_t)F_SLOW)) continue;
+    const uint64_t first = rlo + rc;
+    const uint64_t ps = max(first, x0), pe = min(rlo + rlen, x1);
     if (ps >= pe) continue;
     const int64_t s = q / M;
     unsigned long long *acc = a.acc + s * ACC;
-    if ((*reinterpret_cast<volatile unsigned long long *>(acc + 1) & F_SLOW) != 0ull) continue;
-    const SmemCfg C = smem_cfg(P, a.cfg_idx ? (int)a.cfg_idx[s] : 0);
+    const SmemCfg C = smem_cfg(P, (int)k);
     const GTab G{sbase + C.off_A, sbase + C.off_Bt, 4u * C.r, C.nA1};
     uint64_t tot = 0, srv = 0;
     bool bad = false;
-    stream_piece(a.waits, ps, pe, first, G, lane, tot, bad);
-    const uint64_t se = min(pe, r.lo + min(r.B, r.len));
-    for (uint64_t p = ps + lane; p < se; p += 32u) srv += G(__ldg(a.waits + p));
+    stream_piece(a.waits, ps, pe, first, min(pe, rlo + min(rB, rlen)), G, lane, tot, srv, bad);
     if (__any_sync(FULL, bad) && lane == 0) atomicOr(acc + 1, F_BAD);
     tot = wsum64(tot);
     srv = wsum64(srv);
@@ -264,6 +292,8 @@ __global__ void __launch_bounds__(256, ES_K1_MINB) k1s_stream_fast(const uint8_t
 template <int MM>
 __global__ void __launch_bounds__(256) k1s_stream_slow(const uint8_t *__restrict__ gimg, ImgLayout lay,
                                                        StreamArgs a) {
+  pdl_trigger();
+  pdl_wait();
   const int64_t n_slow = (int64_t)*a.slow_n;  // block-uniform
   if (n_slow == 0) return;
   extern __shared__ __align__(16) uint8_t smem[];
@@ -335,6 +365,7 @@ __global__ void __launch_bounds__(256) k1s_stream_slow(const uint8_t *__restrict
 
 // one 8-lane group per snapshot, lane m = candidate m
 __global__ void __launch_bounds__(256) k1s_finish(const uint8_t *__restrict__ gimg, ImgLayout lay, StreamArgs a) {
+  pdl_wait();
   const CfgRec *cfg = reinterpret_cast<const CfgRec *>(gimg + lay.off_cfg);
   const int M = lay.M;
   const int lane = threadIdx.x & 31, sub = lane >> 3, m = lane & 7;
@@ -404,9 +435,12 @@ __global__ void __launch_bounds__(256) k1s_finish(const uint8_t *__restrict__ gi
   }
 }
 
+// pdl: programmatic dependent launch -- the kernel may start while its
+// predecessor drains; it runs its prologue (image staging, range search) and
+// blocks in pdl_wait() before touching the predecessor's outputs
 template <typename Kern>
 cudaError_t launch_persistent(Kern kern, const uint8_t *img, const ImgLayout &lay, const StreamArgs &a, int64_t items,
-                              int per_block, size_t dyn, cudaStream_t st, int sms) {
+                              int per_block, size_t dyn, cudaStream_t st, int sms, bool pdl = true) {
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
   if (e != cudaSuccess) return e;
   int occ = 0;
@@ -417,8 +451,17 @@ cudaError_t launch_persistent(Kern kern, const uint8_t *img, const ImgLayout &la
   const int64_t cap = (int64_t)sms * occ;
   if (blocks > cap) blocks = cap;
   if (blocks < 1) blocks = 1;
-  kern<<<(unsigned)blocks, 256, dyn, st>>>(img, lay, a);
-  return cudaGetLastError();
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)blocks);
+  cfg.blockDim = dim3(256);
+  cfg.dynamicSmemBytes = dyn;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kern, img, lay, a);
 }
 
 }  // namespace
@@ -451,7 +494,7 @@ cudaError_t launch_score_stream(const uint8_t *img, const ImgLayout &lay, const 
   a.slow_list = reinterpret_cast<int64_t *>(sp + acc_bytes);
   a.rec = reinterpret_cast<QRec *>(sp + acc_bytes + list_bytes);
   e = cudaMemsetAsync(a.acc, 0, acc_bytes, st);
-  if (e == cudaSuccess) e = launch_persistent(k1s_prep, img, lay, a, nq, 256, lay.bytes, st, sms);
+  if (e == cudaSuccess) e = launch_persistent(k1s_prep, img, lay, a, nq, 256, lay.bytes, st, sms, false);
   if (e == cudaSuccess) e = launch_persistent(k1s_stream_fast, img, lay, a, nq, 8, lay.bytes, st, sms);
   if (e == cudaSuccess) {
     if (lay.M <= 2) e = launch_persistent(k1s_stream_slow<2>, img, lay, a, nq, 8, lay.bytes, st, sms);

@@ -31,7 +31,7 @@ with open(os.path.join(P, f"{R}_launches.txt"), "w") as f:
         f.write(f"{k[:60]:60s} {cnt[k]:8d} {v:12.0f} {100 * v / allns:6.1f}%\n")
 
 traffic = {}
-for tag, kern in [("k2", "k2_replay"), ("k3", "k3_scen_p95")]:
+for tag, kern in [("k2", "k2_replay"), ("k3", "k3_stats"), ("k1", "k1_call")]:
     rep = os.path.join(G, f"prof_{tag}_{R}.ncu-rep")
     if not os.path.exists(rep):
         continue
@@ -40,12 +40,20 @@ for tag, kern in [("k2", "k2_replay"), ("k3", "k3_scen_p95")]:
     open(os.path.join(P, f"{R}_ncu_{tag}.txt"), "w").write(s)
     out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rr = list(csv.reader(io.StringIO(out)))
-    hh, uu, vv = rr[0], rr[1], rr[2]
-    def val(m):
-        x = float(vv[hh.index(m)].replace(",", ""))
+    hh, uu = rr[0], rr[1]
+    def val(row, m):
+        x = float(row[hh.index(m)].replace(",", ""))
         u = uu[hh.index(m)]
         return x * {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(u, 1)
-    traffic[kern] = val("dram__bytes_read.sum") + val("dram__bytes_write.sum")
+    total = 0.0
+    for row in rr[2:]:  # one row per captured launch (K1: the four kernels of one call)
+        b = val(row, "dram__bytes_read.sum") + val(row, "dram__bytes_write.sum")
+        name = row[hh.index("Kernel Name")].split("(")[0].split("::")[-1].split("<")[0].strip()
+        name = name.replace("void ", "")
+        if tag == "k1":
+            traffic[name] = b
+        total += b
+    traffic[kern] = total
 json.dump({**traffic, "_source": f"ncu --set full, {R}, dram__bytes_read.sum + dram__bytes_write.sum per launch"},
           open(os.path.join(P, "ncu_traffic.json"), "w"), indent=1)
 print(open(os.path.join(P, f"{R}_launches.txt")).read())

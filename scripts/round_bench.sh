@@ -6,7 +6,10 @@ timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none --csv --lo
   python bench.py --steps 2 --warmup 1 --ncu > /dev/null 2>&1
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:k2_replay -s 1 -c 1 \
   -o gpurun_out/prof_k2_$R python bench.py --steps 1 --warmup 1 --ncu > /dev/null 2>&1
-timeout 600 ncu --set full --clock-control none -k regex:k3_scen_p95 -s 1 -c 1 \
+timeout 600 ncu --set full --clock-control none -k regex:k3_stats -s 1 -c 1 \
   -o gpurun_out/prof_k3_$R python bench.py --steps 1 --warmup 1 --ncu > /dev/null 2>&1
 timeout 200 python bench.py --impl reference --steps 3 --warmup 1 > gpurun_out/bench_ref_$R.json 2>&1
 ls gpurun_out
+# K1 (deep snapshots): the four kernels of the second es_score_candidates call of the probe
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:k1s_ -s 4 -c 4 \
+  -o gpurun_out/prof_k1_$R python scripts/k1_probe.py stream > /dev/null 2>&1
