@@ -104,6 +104,52 @@ def test_k1_deep_snapshots(M, depth):
     assert_k1_equal(run_k1(prof, cfgs, q_off, w), oracle.decide_batch(prof, cfgs, q_off, w), M)
 
 
+@pytest.mark.parametrize("base_off", [0, 1, 3])
+def test_k1_stream_live_windows(monkeypatch, base_off):
+    """The streaming mapping on all-live deep queues (the HBM regime of the
+    bench): warp ranges cut queues at arbitrary positions, the waits pointer is
+    misaligned by base_off elements (scalar heads/tails around the 16-byte
+    body), B* up to 64 (served heads longer than a warp), two SLOs, a few
+    clip-path snapshots mixed in, and inversions planted in bodies, at 16-byte
+    boundaries and in the last wait of a queue (flagged bad, Q24)."""
+    monkeypatch.setenv("ES_K1", "stream")
+    M = 8
+    prof = inputs.synth_profile(M, 5, list(range(1, 65)))
+    cfgs = [inputs.SchedCfg(tau=50000, b_max=64), inputs.SchedCfg(tau=80000, b_max=40)]
+    n = 600
+    q_off, w = inputs.snapshots_poisson_depth(11, np.arange(n), M, 1500, [1500 / 100000.0] * M)
+    w = w.copy()
+    rng = np.random.default_rng(5)
+    # clip path: push the head of a few snapshots near x_c
+    clip = rng.choice(n, 20, replace=False)
+    for s in clip:
+        lo, hi = int(q_off[s * M]), int(q_off[s * M + 1])
+        if hi > lo:
+            w[lo] = max(int(w[lo]), 170000)
+    # inversions: body, 16-byte boundary, last wait of a queue
+    planted = []
+    for s in rng.choice(np.setdiff1d(np.arange(n), clip), 12, replace=False):
+        m = int(rng.integers(M))
+        lo, hi = int(q_off[s * M + m]), int(q_off[s * M + m + 1])
+        if hi - lo < 10:
+            continue
+        pos = [lo + (hi - lo) // 2, (lo + 5) & ~3, hi - 1][len(planted) % 3]
+        pos = min(max(pos, lo + 1), hi - 1)
+        w[pos] = w[pos - 1] + 1
+        planted.append(s)
+    ci = (np.arange(n) % 2).astype(np.uint16)
+    h = es.es_load_profile(prof, cfgs)
+    buf = np.zeros(w.size + base_off, np.uint32)
+    buf[base_off:] = w
+    dw = to_dev(buf, torch.uint32)[base_off:]
+    o = es.es_score_candidates(h, to_dev(q_off, torch.uint64), dw, to_dev(ci, torch.uint16))
+    torch.cuda.synchronize()
+    g = {k: np_of(v) for k, v in o.items()}
+    ref = oracle.decide_batch(prof, cfgs, q_off, w, ci)
+    assert_k1_equal(g, ref, M)
+    assert (ref["flags"][planted] & 4).all()  # every planted inversion is in the read window
+
+
 def test_k1_masks_and_flags():
     """exit masks (ablation), no-work, bad input, bad cfg index."""
     prof = inputs.synth_profile(3, 4, [1, 2, 4, 8])
