@@ -77,15 +77,6 @@ __device__ uint32_t find_bin(const T *hist, int nbins, uint64_t k, uint64_t *bef
   return b;
 }
 
-// shared-memory histogram add, aggregated across a warp's lanes with the same bin
-__device__ __forceinline__ void hist_add(uint32_t *hist, bool take, uint32_t bin) {
-  const unsigned act = __ballot_sync(0xffffffffu, take);
-  if (take) {
-    const unsigned peers = __match_any_sync(act, bin);
-    if ((threadIdx.x & 31) == (unsigned)(__ffs(peers) - 1)) atomicAdd(&hist[bin], (uint32_t)__popc(peers));
-  }
-}
-
 struct StatsArgs {
   int64_t n_scen;
   int M;
@@ -106,6 +97,14 @@ __global__ void __launch_bounds__(NT) k3_stats(StatsArgs a) {
   __shared__ uint32_t hist[BINS];
   __shared__ uint32_t s_max;
   extern __shared__ __align__(16) uint32_t vals[];
+  __shared__ uint64_t mbar;
+  const uint32_t mb = (uint32_t)__cvta_generic_to_shared(&mbar);
+  uint32_t phase = 0;
+  if (threadIdx.x == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(mb));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
   for (int64_t s = blockIdx.x; s < a.n_scen; s += gridDim.x) {
     const uint64_t *st = a.stats + s * ES_NSTAT;
     const int k = a.cfg_idx ? (int)a.cfg_idx[s] : 0;
@@ -131,60 +130,104 @@ __global__ void __launch_bounds__(NT) k3_stats(StatsArgs a) {
     }
     const uint32_t *gsrc = a.lat + base + W;
     const bool staged = n <= a.cap;
+    // stage the scenario's latencies into shared memory with TMA: one bulk copy
+    // of the 16-byte aligned span [gsrc - off, ...) (off <= 3 leading words
+    // ignored), the <= 3 trailing words loaded directly
+    const uint32_t *src = gsrc;
+    if (staged) {
+      const uint32_t off = (uint32_t)(((uintptr_t)gsrc >> 2) & 3u);
+      const uint32_t nv4 = (n + off) / 4u;
+      if (threadIdx.x == 0 && nv4) {
+        // the previous scenario's generic-proxy reads of vals precede these async writes
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(mb), "r"(16u * nv4) : "memory");
+        const uint32_t dst = (uint32_t)__cvta_generic_to_shared(vals);
+        const uint8_t *gs = reinterpret_cast<const uint8_t *>(gsrc - off);
+        for (uint32_t o = 0; o < 16u * nv4; o += 16384u)
+          asm volatile(
+              "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                  dst + o),
+              "l"(gs + o), "r"(min(16384u, 16u * nv4 - o)), "r"(mb)
+              : "memory");
+      }
+      for (uint32_t j = 4u * nv4 + threadIdx.x; j < n + off; j += NT) vals[j] = gsrc[j - off];
+      if (nv4) {
+        uint32_t done = 0;
+        while (!done)
+          asm volatile(
+              "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+              "selp.u32 %0, 1, 0, p;\n\t}"
+              : "=r"(done)
+              : "r"(mb), "r"(phase)
+              : "memory");
+        phase ^= 1u;
+      }
+      src = vals + off;
+    }
+    // pass A: coarse histogram min(T >> 12, 4095) -- the group level-0 digit,
+    // and the first digit of the scenario's own selection
+    for (int i = threadIdx.x; i < BINS; i += NT) hist[i] = 0u;
     if (threadIdx.x == 0) s_max = 0u;
-    __syncthreads();
+    __syncthreads();  // staged tail words and the zeroed histogram are visible
     uint32_t mx = 0;
-    for (uint32_t i = threadIdx.x; i < n; i += NT) {
-      const uint32_t v = gsrc[i];
-      if (staged) vals[i] = v;
+    for (uint32_t i0 = 0; i0 < n; i0 += NT) {
+      const uint32_t i = i0 + threadIdx.x;
+      const bool take = i < n;
+      const uint32_t v = take ? src[i] : 0u;
       mx = max(mx, v);
+      if (take) atomicAdd(&hist[min(v >> 12, COARSE_OVF)], 1u);
     }
     mx = __reduce_max_sync(0xffffffffu, mx);
     if ((threadIdx.x & 31) == 0) atomicMax(&s_max, mx);
     __syncthreads();
     const uint32_t vmax = s_max;
-    const uint32_t *src = staged ? vals : gsrc;
-    if (a.p95) {
-      const uint32_t nbits = 32u - __clz(vmax);
-      uint32_t prev = nbits;  // bits >= prev already selected (hv)
-      uint32_t shift = nbits > 12u ? nbits - 12u : 0u;
-      uint64_t kk = (95ull * n + 99ull) / 100ull;  // ceil(0.95 n), 1-based rank
-      uint64_t hv = 0;
-      for (;;) {
-        const uint32_t nb = 1u << (prev - shift);
-        for (uint32_t i = threadIdx.x; i < nb; i += NT) hist[i] = 0u;
-        __syncthreads();
-        const uint32_t dmask = nb - 1u;
-        for (uint32_t i = threadIdx.x; i < n; i += NT) {
-          const uint32_t v = src[i];
-          if (((uint64_t)v >> prev) == hv) atomicAdd(&hist[(v >> shift) & dmask], 1u);
-        }
-        __syncthreads();
-        uint64_t before;
-        const uint32_t b = find_bin(hist, (int)nb, kk, &before);
-        kk -= before;
-        hv = (hv << (prev - shift)) | b;
-        if (shift == 0u) break;
-        prev = shift;
-        shift = shift > 12u ? shift - 12u : 0u;
-      }
-      if (threadIdx.x == 0) a.p95[s] = (uint32_t)hv;
-      __syncthreads();
-    }
-    if (grp) {  // level-0 coarse histogram of the group, bins [0, top]
-      const uint32_t top = min(vmax >> 12, COARSE_OVF);
-      for (uint32_t i = threadIdx.x; i <= top; i += NT) hist[i] = 0u;
-      __syncthreads();
-      for (uint32_t i0 = 0; i0 < n; i0 += NT) {  // whole warps iterate together (ballot inside)
-        const uint32_t i = i0 + threadIdx.x;
-        const bool take = i < n;
-        const uint32_t v = take ? src[i] : 0u;
-        hist_add(hist, take, min(v >> 12, COARSE_OVF));
-      }
-      __syncthreads();
+    const uint32_t top = min(vmax >> 12, COARSE_OVF);
+    if (grp) {  // flush the coarse histogram into the group's level-0 histogram
       unsigned long long *gh = reinterpret_cast<unsigned long long *>(a.hist0 + (uint64_t)g * BINS);
       for (uint32_t i = threadIdx.x; i <= top; i += NT)
         if (hist[i]) atomicAdd(gh + i, (unsigned long long)hist[i]);
+    }
+    if (a.p95) {
+      uint64_t kk = (95ull * n + 99ull) / 100ull;  // ceil(0.95 n), 1-based rank
+      uint64_t before;
+      const uint32_t cb = find_bin(hist, (int)top + 1, kk, &before);  // syncs: flush reads done
+      uint32_t res;
+      if (cb < COARSE_OVF) {  // pass B: T & 0xFFF inside the coarse bin -> exact value
+        kk -= before;
+        for (int i = threadIdx.x; i < BINS; i += NT) hist[i] = 0u;
+        __syncthreads();
+        for (uint32_t i = threadIdx.x; i < n; i += NT) {
+          const uint32_t v = src[i];
+          if ((v >> 12) == cb) atomicAdd(&hist[v & 0xFFFu], 1u);
+        }
+        __syncthreads();
+        const uint32_t fb = find_bin(hist, BINS, kk, &before);
+        res = (cb << 12) | fb;
+      } else {  // the rank falls among T >= 16.77 s: radix select from the top bit
+        const uint32_t nbits = 32u - __clz(vmax);
+        uint32_t prev = nbits;  // bits >= prev already selected (hv)
+        uint32_t shift = nbits > 12u ? nbits - 12u : 0u;
+        uint64_t hv = 0;
+        for (;;) {
+          const uint32_t nb = 1u << (prev - shift);
+          for (uint32_t i = threadIdx.x; i < nb; i += NT) hist[i] = 0u;
+          __syncthreads();
+          const uint32_t dmask = nb - 1u;
+          for (uint32_t i = threadIdx.x; i < n; i += NT) {
+            const uint32_t v = src[i];
+            if (((uint64_t)v >> prev) == hv) atomicAdd(&hist[(v >> shift) & dmask], 1u);
+          }
+          __syncthreads();
+          const uint32_t bb = find_bin(hist, (int)nb, kk, &before);
+          kk -= before;
+          hv = (hv << (prev - shift)) | bb;
+          if (shift == 0u) break;
+          prev = shift;
+          shift = shift > 12u ? shift - 12u : 0u;
+        }
+        res = (uint32_t)hv;
+      }
+      if (threadIdx.x == 0) a.p95[s] = res;
     }
     __syncthreads();
   }
@@ -229,7 +272,7 @@ __global__ void __launch_bounds__(NT) k_group_level(GroupArgs a) {
     const uint32_t *src = a.lat + base + W;
     for (int i = threadIdx.x; i < BINS; i += NT) hist[i] = 0u;
     __syncthreads();
-    for (uint32_t i0 = 0; i0 < n; i0 += NT) {  // whole warps iterate together (ballot inside)
+    for (uint32_t i0 = 0; i0 < n; i0 += NT) {
       const uint32_t i = i0 + threadIdx.x;
       const uint32_t v = i < n ? src[i] : 0u;
       uint32_t bin = 0;
@@ -249,7 +292,7 @@ __global__ void __launch_bounds__(NT) k_group_level(GroupArgs a) {
           bin = v & 0xFFu;
         }
       }
-      hist_add(hist, take, bin);
+      if (take) atomicAdd(&hist[bin], 1u);
     }
     __syncthreads();
     unsigned long long *gh = reinterpret_cast<unsigned long long *>(a.hist + (uint64_t)g * BINS);
