@@ -302,14 +302,17 @@ __device__ __forceinline__ Decision finish_decision(const Seg<LPS, MM> &sg, cons
   constexpr int GL = Seg<LPS, MM>::GL;
   const uint64_t S_own = Sq;
   constexpr uint64_t LIM = 1ull << 61;
-  if (!__any_sync(FULL, mkey != 0xFFu && Sq >= LIM)) {
-    // key = S * 8 + m orders exactly like (S, m) while S < 2^61; empty -> max
-    uint64_t key = mkey == 0xFFu ? ~0ull : ((Sq << 3) | mkey);
+  // key = S * 8 + m orders exactly like (S, m) while S < 2^61; empty -> max.
+  // The packed argmin runs unconditionally (the vote on S >= 2^61 overlaps
+  // it); the wide (S, m) argmin redoes it only if some score is that large.
+  const bool wide = __any_sync(FULL, mkey != 0xFFu && Sq >= LIM);
+  uint64_t key = mkey == 0xFFu ? ~0ull : ((Sq << 3) | mkey);
 #pragma unroll
-    for (int o = GL; o < LPS; o <<= 1) {
-      const uint64_t ko = __shfl_xor_sync(FULL, key, o, LPS);
-      key = ko < key ? ko : key;
-    }
+  for (int o = GL; o < LPS; o <<= 1) {
+    const uint64_t ko = __shfl_xor_sync(FULL, key, o, LPS);
+    key = ko < key ? ko : key;
+  }
+  if (!wide) {
     if (key != ~0ull) {
       Sq = key >> 3;
       mkey = (uint32_t)(key & 7u);
@@ -423,9 +426,10 @@ __device__ __forceinline__ Decision decide_general(const Seg<LPS, MM> &sg, const
 // result, and wait_at(p) returning the wait of position p (c <= p < len; no
 // warp-synchronous operation inside).  Returns the segment's decision
 // (uniform across the segment).  Empty groups / inactive segments: len = 0.
+// fast: no head wait of the warp reaches x_c - max L (warp-uniform; see below).
 template <int LPS, int MM, class WaitAt>
 __device__ __forceinline__ Decision decide(const Seg<LPS, MM> &sg, const SmemProf &P, const SmemCfg &C,
-                                           uint32_t len, uint32_t c, uint32_t wmax, const Cand &cand,
+                                           uint32_t len, uint32_t c, bool fast, const Cand &cand,
                                            WaitAt wait_at) {
   constexpr int GL = Seg<LPS, MM>::GL;
   const uint32_t Bown = len ? cand.B : 0u;
@@ -435,7 +439,7 @@ __device__ __forceinline__ Decision decide(const Seg<LPS, MM> &sg, const SmemPro
   // task of any queue can reach x_c under any candidate's prediction, so
   // K_m = 0 and U_m = sum_all G - sum_{own served} G for every m.  The
   // per-candidate clip tests and 3 M reductions collapse to 4 reductions.
-  if (!__any_sync(FULL, len > 0u && wmax >= C.fast_lim)) {
+  if (fast) {
     uint64_t tot = 0ull, srv = 0ull;
     // WU positions per lane per step: their loads issue back to back (the
     // per-decision chain is latency-bound, one queue is a handful of steps)

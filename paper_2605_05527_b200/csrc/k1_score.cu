@@ -80,7 +80,8 @@ __global__ void __launch_bounds__(256) k1_score(const uint8_t *__restrict__ gimg
     const uint32_t c = srch ? phi : 0u;
     const Cand cand = cand_params<LPS, MM>(sg, P, C, len, wmax);
     bool bad = false;
-    const Decision d = decide<LPS, MM>(sg, P, C, len, c, wmax, cand, [&](uint32_t p) {
+    const bool fast = !__any_sync(FULL, len > 0u && wmax >= C.fast_lim);
+    const Decision d = decide<LPS, MM>(sg, P, C, len, c, fast, cand, [&](uint32_t p) {
       const uint32_t w = __ldg(W + p);
       // read-window validation: head-first waits must not increase (Q7)
       if (p > c && w > __ldg(W + p - 1)) bad = true;

@@ -58,6 +58,18 @@ __device__ __forceinline__ uint32_t ldg_u32(const uint32_t *p) { return __ldg(p)
 // L1 prefetch of an upcoming arrival line (admission reads it a few decisions later)
 __device__ __forceinline__ void prefetch_l1(const uint32_t *p) { asm volatile("prefetch.global.L1 [%0];" ::"l"(p)); }
 
+// some segment is running (go) with all its queues empty: per-segment test of two ballots
+template <int LPS>
+__device__ __forceinline__ bool segs_idle(unsigned b_go, unsigned b_has) {
+  bool idle = false;
+#pragma unroll
+  for (int k = 0; k < 32 / LPS; ++k) {
+    const unsigned m = (LPS == 32 ? 0xFFFFFFFFu : ((1u << LPS) - 1u)) << (k * LPS);
+    idle |= (b_go & m) != 0u && (b_has & m) == 0u;
+  }
+  return idle;
+}
+
 __device__ __forceinline__ void report(DevStatus *ds, uint32_t code, int64_t item) {
   if (atomicCAS(&ds->code, 0u, code) == 0u) ds->item = (unsigned long long)item;
 }
@@ -177,19 +189,26 @@ __global__ void __launch_bounds__(256) k2_replay(const uint8_t *__restrict__ gim
       }
       const bool go = run && status == ES_OK;
       uint32_t len = go ? tail - head : 0u;
-      const bool has = sg.seg_any(len > 0u);
-      if (__any_sync(FULL, go && !has)) {  // idle GPU: jump to the next arrival (Q12)
+      // a3/a4 inputs: head wait (issued before admission), clipped-for-everyone prefix
+      const uint32_t ahead = len == 0u ? t : (pre_ok ? ahead_pre : ldg_u32(Aq + head));
+      uint32_t wmax = t - ahead;
+      // every warp-uniform decision of this step from one round of independent
+      // ballots (they pipeline; a chain of votes would not)
+      const unsigned b_go = __ballot_sync(FULL, go);
+      const unsigned b_has = __ballot_sync(FULL, len > 0u);
+      const unsigned b_xc = __ballot_sync(FULL, len > 0u && wmax >= C.x_c);
+      const unsigned b_slow = __ballot_sync(FULL, len > 0u && wmax >= C.fast_lim);
+      const bool has = sg.sbits(b_has) != 0u;
+      // idle GPU (Q12): a running segment with every queue empty jumps to the next arrival
+      if (segs_idle<LPS>(b_go, b_has)) {
         const uint32_t tn = sg.vmin(go ? next_arr : 0xFFFFFFFFu);
         if (go && !has) t = tn;
       }
       const bool dec = go && has;
       if (!dec) len = 0u;
       maxd = max(maxd, len);
-      // a3/a4 inputs: head wait, clipped-for-everyone prefix
-      const uint32_t ahead = len == 0u ? t : (pre_ok ? ahead_pre : ldg_u32(Aq + head));
-      const uint32_t wmax = t - ahead;
       if (live < head) live = head;
-      if (__any_sync(FULL, len > 0u && wmax >= C.x_c)) {
+      if (b_xc != 0u) {
         bool adv = true;
         while (adv) {
           const uint32_t idx = live + sg.gl;
@@ -204,7 +223,7 @@ __global__ void __launch_bounds__(256) k2_replay(const uint8_t *__restrict__ gim
       const uint32_t tt = t;
       const uint32_t *Ah = Aq + head;
       const Decision d =
-          decide<LPS, MM>(sg, P, C, len, c, wmax, cand, [&](uint32_t p) { return tt - ldg_u32(Ah + p); });
+          decide<LPS, MM>(sg, P, C, len, c, b_slow == 0u, cand, [&](uint32_t p) { return tt - ldg_u32(Ah + p); });
       const uint32_t ncand = __popc(sg.sbits(__ballot_sync(FULL, sg.gl == 0 && len > 0u)));
       // a8: commit
       const int src = (int)(d.m & (MM - 1)) * GL;
