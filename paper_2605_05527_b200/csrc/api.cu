@@ -179,6 +179,14 @@ es_status es_load_profile(const es_profile_desc *desc, const es_sched_cfg *cfgs,
     r.status = 0xFFFFFFFFu;
   }
   lay.bytes = off;
+  {
+    uint32_t p2 = 1;
+    while (p2 < recs[0].nA_cap) p2 <<= 1;
+    lay.c0_offA = recs[0].off_A;
+    lay.c0_offBt = recs[0].off_Bt;
+    lay.c0_r4 = 4u * ((1024u - recs[0].tau % 1024u) % 1024u);
+    lay.c0_amask = 4u * (p2 - 1u);
+  }
   const int smax = max_dyn_smem(device);
   if ((int)lay.bytes + 64 > smax)
     return fail(ES_ERR_ARG, "profile image of %u bytes exceeds %d bytes of shared memory per CTA (too many cfgs)",

@@ -36,6 +36,10 @@ struct ImgLayout {
   uint32_t bytes;  // total, multiple of 16
   int32_t M, E, nb, ncfg;
   uint32_t off_lat, off_bs, off_mask, off_cfg;
+  // cfg 0's urgency-table constants (host-computed), kernel parameters for the
+  // single-SLO specialisation of the K1 stream: byte offsets of A and Bt, 4 r,
+  // and the A index mask 4 (2^k - 1) with 2^k >= nA_cap
+  uint32_t c0_offA, c0_offBt, c0_r4, c0_amask;
 };
 
 // device-side sticky error record (per profile handle)

@@ -19,6 +19,9 @@
 // Scratch (records + accumulators) is stream-ordered (cudaMallocAsync).
 #include <cuda_runtime.h>
 
+#include <cstdlib>
+#include <cstring>
+
 #include "decide.cuh"
 
 namespace es {
@@ -28,6 +31,7 @@ struct QRec {  // per (snapshot, model) queue
   uint64_t lo;
   uint64_t H;
   uint32_t len, c, B, thr, L, ef;  // ef = e | feasible << 7
+  uint64_t srv;                    // fast path: sum of G over the own served head [0, min(B*, len))
 };
 
 constexpr int ACC = 2 + 2 * MAXM;  // tot, flags, S-part[8] (srv or U), K[8]
@@ -105,6 +109,12 @@ __global__ void __launch_bounds__(256) k1s_prep(const uint8_t *__restrict__ gimg
       r.ef = e | (best >= 0 ? 0x80u : 0u);
       r.thr = r.L < C.x_c ? C.x_c - r.L : 0u;
       r.H = r.L < C.x_c ? reinterpret_cast<const uint64_t *>(P.sm + C.off_H)[((size_t)g * P.E + e) * P.nb + bi] : 0ull;
+      // own served head for the fast path (the clip path excludes it per task)
+      const uint32_t nsv = r.B < r.len ? r.B : r.len;
+      uint64_t sv = G_of(P, C, wmax);
+#pragma unroll 8
+      for (uint32_t j = 1; j < nsv; ++j) sv += G_of(P, C, __ldg(W + j));
+      r.srv = sv;
       if (wmax >= C.fast_lim || C.x_c > V4_LIM) {
         const unsigned long long was = atomicOr(a.acc + s * ACC + 1, F_SLOW);
         if (!(was & F_SLOW)) a.slow_list[atomicAdd(a.slow_n, 1ull)] = s;
@@ -248,7 +258,7 @@ __global__ void __launch_bounds__(256, ES_K1_MINB) k1s_stream_fast(const uint8_t
   // queue descriptors spread over the lanes (lane l < 10: word l of the QRec,
   // lane 10: the snapshot's flag word, lane 11: its SLO index), fetched one
   // piece ahead so the next piece's record is in flight while this one streams
-  static_assert(sizeof(QRec) == 40, "QRec");
+  static_assert(sizeof(QRec) == 48, "QRec");  // words 0..9 fetched; srv is read by k1s_finish
   auto fetch = [&](int64_t q) -> uint32_t {
     if (q >= nq) return 0u;
     const int64_t s = q / M;
@@ -277,7 +287,7 @@ __global__ void __launch_bounds__(256, ES_K1_MINB) k1s_stream_fast(const uint8_t
     const GTab G{sbase + C.off_A, sbase + C.off_Bt, 4u * C.r, C.nA1};
     uint64_t tot = 0, srv = 0;
     bool bad = false;
-    stream_piece(a.waits, ps, pe, first, min(pe, rlo + min(rB, rlen)), G, lane, tot, srv, bad);
+    stream_piece(a.waits, ps, pe, first, ps, G, lane, tot, srv, bad);  // served heads: k1s_finish
     if (__any_sync(FULL, bad) && lane == 0) atomicOr(acc + 1, F_BAD);
     tot = wsum64(tot);
     srv = wsum64(srv);
@@ -286,6 +296,307 @@ __global__ void __launch_bounds__(256, ES_K1_MINB) k1s_stream_fast(const uint8_t
       if (srv) atomicAdd(acc + 2 + (q - s * M), (unsigned long long)srv);
     }
   }
+}
+
+// ---------------------------------------------------------------------------
+// fast path, TMA form: the flat waits array is cut into one contiguous range of
+// 16-byte vectors per warp (equal bytes per warp).  Each warp owns a ring of
+// NSL shared-memory slots of PV vectors; its lane 0 keeps NSL-1 pieces of the
+// range in flight with cp.async.bulk (one mbarrier per slot), so the HBM
+// stream never restarts at queue boundaries and needs no registers for the
+// bytes in flight.  The warp walks its range one 128-wait window at a time
+// with a warp-uniform queue state (current queue record, the next one
+// prefetched): a window strictly inside the live, unserved part of a fast
+// queue takes the 4-waits-per-lane fast body; any other window (queue or
+// snapshot boundary, served head, range end) goes through the
+// element-wise handler.  Per-snapshot totals and per-queue served sums are
+// warp-reduced and added with one u64 atomic per snapshot / queue.
+constexpr uint32_t PV_MAX = 256;  // vectors (16 B) per piece: 4 KB (2 KB for large profile images)
+
+struct TmaRing {
+  uint32_t pv;        // vectors per piece (slot size 16 pv bytes)
+  uint32_t nsl;       // slots per warp
+  uint32_t ring_off;  // byte offset of the rings in dynamic smem
+  uint32_t mbar_off;  // byte offset of the mbarriers
+};
+
+__device__ __forceinline__ void mbar_init(uint32_t mb, uint32_t cnt) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(mb), "r"(cnt));
+}
+__device__ __forceinline__ void mbar_wait(uint32_t mb, uint32_t parity) {
+  uint32_t done = 0;
+  while (!done) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(done)
+        : "r"(mb), "r"(parity)
+        : "memory");
+  }
+}
+__device__ __forceinline__ uint4 lds_v4(uint32_t saddr) {
+  uint4 v;
+  asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+               : "r"(saddr));
+  return v;
+}
+
+__device__ __forceinline__ uint64_t wsum64_u(uint64_t v) {
+  const uint32_t lo = (uint32_t)v, hi = (uint32_t)(v >> 32);
+  // lo sum needs 37 bits: split into 16-bit halves to keep REDUX exact
+  const uint64_t l0 = redux_add(lo & 0xFFFFu), l1 = redux_add(lo >> 16);
+  const uint64_t h = redux_add(hi);
+  return l0 + (l1 << 16) + (h << 32);
+}
+
+// G(w) of the single-SLO specialisation: the table bases are kernel
+// parameters (uniform registers, folded into the LDS address), the A index is
+// masked to the table's power-of-two capacity (exact for w < x_c; an inverted
+// input reads an in-bounds garbage value and is flagged bad)
+struct GOne {
+  uint32_t sA, sBt, r4, amask;
+  __device__ __forceinline__ uint32_t operator()(uint32_t w) const {
+    const uint32_t v4 = w * 4u + r4;
+    const uint32_t a = lds_u32(sA + ((v4 >> SBITS) & amask));
+    const uint32_t b = lds_u32(sBt + (v4 & (4u * S - 4u)));
+    return (uint32_t)(((uint64_t)a * (uint64_t)b) >> F);
+  }
+};
+
+template <bool ONE, int TMA_NW>
+__global__ void __launch_bounds__(TMA_NW * 32, 1) k1s_stream_tma(const uint8_t *__restrict__ gimg, ImgLayout lay,
+                                                                 StreamArgs a, TmaRing rg) {
+  pdl_trigger();
+  extern __shared__ __align__(16) uint8_t smem[];
+  __shared__ uint64_t mbar;
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(smem);
+  const uint32_t PV = rg.pv;
+  const uint32_t ring = sbase + rg.ring_off + (uint32_t)wib * rg.nsl * (PV * 16u);
+  const uint32_t bars = sbase + rg.mbar_off + (uint32_t)wib * rg.nsl * 8u;
+  const int M = lay.M;
+  const int64_t nq = a.n * M;
+  // ---- this warp's vector range (vector 0 = the 16-byte unit holding waits[base])
+  const uint64_t base = nq ? __ldg(a.q_off) : 0ull, end = nq ? __ldg(a.q_off + nq) : 0ull;
+  const uintptr_t ga = reinterpret_cast<uintptr_t>(a.waits);
+  const uintptr_t vaddr = (ga + 4u * base) & ~(uintptr_t)15u;
+  const int64_t pv0 = (int64_t)base - (int64_t)(((ga + 4u * base) & 15u) >> 2);  // position of vector 0, lane 0
+  const uint64_t bytes_end = ga + 4u * end - vaddr;
+  const int64_t nvec = end > base ? (int64_t)((bytes_end + 15u) >> 4) : 0;
+  const int64_t nfull = end > base ? (int64_t)(bytes_end >> 4) : 0;  // vectors wholly inside the array
+  const int64_t nwarps = (int64_t)gridDim.x * TMA_NW;
+  const int64_t vper = ((nvec + nwarps - 1) / nwarps + 31) & ~31ll;
+  const int64_t gw = (int64_t)blockIdx.x * TMA_NW + wib;
+  const int64_t v0 = gw * vper, v1 = min(v0 + vper, nvec);
+  const int64_t npieces = v1 > v0 ? (v1 - v0 + PV - 1) / PV : 0;
+  const uint8_t *gsrc = reinterpret_cast<const uint8_t *>(vaddr);
+  // piece k into `slot`: executed by the whole warp with warp-uniform operands,
+  // one elected lane arms the slot's mbarrier and issues the bulk copy
+  auto issue = [&](int64_t k, uint32_t slot) {
+    const int64_t vs = v0 + k * (int64_t)PV;
+    const int64_t vf = min(min(vs + (int64_t)PV, v1), nfull);
+    const uint32_t nb = vf > vs ? (uint32_t)(vf - vs) * 16u : 0u;
+    const uint32_t mb = bars + 8u * slot;
+    asm volatile(
+        "{\n\t.reg .pred e, c;\n\t"
+        "elect.sync _|e, 0xffffffff;\n\t"
+        "@e mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n\t"
+        "setp.ne.and.u32 c, %1, 0, e;\n\t"
+        "@c cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%2], [%3], %1, [%0];\n\t}" ::"r"(mb),
+        "r"(nb), "r"(ring + slot * (PV * 16u)), "l"(gsrc + vs * 16)
+        : "memory");
+  };
+  if (lane == 0) {
+    for (uint32_t i = 0; i < rg.nsl; ++i) mbar_init(bars + 8u * i, 1u);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncwarp();
+  for (int64_t k = 0; k < min((int64_t)rg.nsl - 1, npieces); ++k) issue(k, (uint32_t)k);
+  stage_image(smem, gimg, lay.bytes, &mbar);  // (also publishes the mbarrier inits)
+  if (npieces == 0) return;
+  const SmemProf P = smem_prof(smem, lay);
+  // ---- initial queue: largest q < nq with q_off[q] <= first position of the range
+  const int64_t R0 = pv0 + 4 * v0;  // range-relative positions are int32 offsets from R0
+  const uint64_t x0 = (uint64_t)max(R0, (int64_t)base);
+  int64_t lo = 0, hi = nq;
+  while (hi - lo > 1) {
+    const int64_t step = (hi - lo + 31) / 32;
+    const int64_t pr = lo + step * lane;
+    const bool ok = pr < hi && __ldg(a.q_off + pr) <= x0;
+    const int l = 31 - __clz(__ballot_sync(FULL, ok));
+    lo += step * l;
+    hi = min(hi, lo + step);
+  }
+  // queue record q of snapshot s spread over the lanes (see k1s_stream_fast)
+  auto fetch = [&](int64_t q, int64_t s) -> uint32_t {
+    if (q >= nq) return 0u;
+    if (lane < 10) return __ldg(reinterpret_cast<const uint32_t *>(a.rec + q) + lane);
+    if (lane == 10) return (uint32_t)a.acc[s * ACC + 1];  // F_SLOW is final (set by k1s_prep)
+    if (lane == 11) return a.cfg_idx ? (uint32_t)a.cfg_idx[s] : 0u;
+    return 0u;
+  };
+  pdl_wait();  // k1s_prep's records and flags
+  constexpr int32_t BIG = 0x3FFFFFFF;
+  const int32_t rend_full = (int32_t)(4 * (min(v1, nfull) - v0));  // fast windows end here
+  int64_t qi = lo, s_cur = lo / M;
+  int m_cur = (int)(lo - s_cur * M);
+  uint32_t dnext = m_cur + 1 < M ? fetch(qi + 1, s_cur) : fetch(qi + 1, s_cur + 1);
+  // warp-uniform queue state (range-relative positions)
+  int32_t qs_r = 0, qe_r = 0, lo_r = BIG, hi_r = -BIG;
+  bool skip = true;
+  GTab Gg{0u, 0u, 0u, 0u};
+  const GOne G1{sbase + lay.c0_offA, sbase + lay.c0_offBt, lay.c0_r4, lay.c0_amask};
+  auto clampr = [&](int64_t p) -> int32_t { return (int32_t)max(min(p - R0, (int64_t)BIG), -(int64_t)BIG); };
+  auto set_queue = [&](uint32_t d, bool new_snap) {
+    const uint64_t rlo = (uint64_t)__shfl_sync(FULL, d, 0) | ((uint64_t)__shfl_sync(FULL, d, 1) << 32);
+    const uint32_t rlen = __shfl_sync(FULL, d, 4);
+    const uint32_t flg = __shfl_sync(FULL, d, 10), k = __shfl_sync(FULL, d, 11);
+    if (!ONE && new_snap && k < (uint32_t)P.ncfg) {
+      const SmemCfg C = smem_cfg(P, (int)k);
+      Gg = GTab{sbase + C.off_A, sbase + C.off_Bt, 4u * C.r, C.nA1};
+    }
+    // rec is zero for an out-of-range cfg (k1s_prep): rlen = 0, the queue is skipped
+    skip = (flg & (uint32_t)F_SLOW) != 0u || rlen == 0u || k >= (uint32_t)P.ncfg;
+    qs_r = clampr((int64_t)rlo);
+    qe_r = clampr((int64_t)(rlo + rlen));
+    lo_r = skip ? BIG : qs_r + 1;
+    hi_r = min(qe_r, rend_full) - 128;
+  };
+  set_queue(fetch(qi, s_cur), true);
+  uint64_t tot = 0;
+  uint32_t bad = 0u;
+  auto Gv = [&](uint32_t w) -> uint32_t { return ONE ? G1(w) : Gg(w); };
+  auto flush_snap = [&]() {
+    const uint64_t v = wsum64_u(tot);
+    const bool b = __any_sync(FULL, bad != 0u);
+    if (lane == 0) {
+      if (v) atomicAdd(a.acc + s_cur * ACC, (unsigned long long)v);
+      if (b) atomicOr(a.acc + s_cur * ACC + 1, F_BAD);
+    }
+    tot = 0;
+    bad = 0u;
+  };
+  auto advance = [&]() {
+    ++qi;
+    if (qi >= nq) {
+      skip = true;
+      qs_r = qe_r = BIG;
+      lo_r = BIG;
+      return;
+    }
+    const uint32_t d = dnext;
+    const bool ns = ++m_cur == M;
+    if (ns) {
+      flush_snap();
+      m_cur = 0;
+      ++s_cur;
+    }
+    dnext = m_cur + 1 < M ? fetch(qi + 1, s_cur) : fetch(qi + 1, s_cur + 1);
+    set_queue(d, ns);
+  };
+  // one fast window: 32 vectors (128 waits) of one live, unserved queue range
+  auto fast_window = [&](const uint4 &x, uint32_t &carry) {
+    uint32_t prev = __shfl_up_sync(FULL, x.w, 1);
+    if (lane == 0) prev = carry;
+    carry = __shfl_sync(FULL, x.w, 31);
+    // Q24 read-window check as one predicate chain: bad = 1 if any wait exceeds its predecessor
+    asm("{\n\t.reg .pred p;\n\t"
+        "setp.gt.u32 p, %1, %2;\n\t"
+        "setp.gt.or.u32 p, %3, %1, p;\n\t"
+        "setp.gt.or.u32 p, %4, %3, p;\n\t"
+        "setp.gt.or.u32 p, %5, %4, p;\n\t"
+        "selp.u32 %0, 1, %0, p;\n\t}"
+        : "+r"(bad)
+        : "r"(x.x), "r"(prev), "r"(x.y), "r"(x.z), "r"(x.w));
+    tot += (uint64_t)Gv(x.x) + Gv(x.y) + (uint64_t)Gv(x.z) + Gv(x.w);
+  };
+  uint32_t carry = R0 > (int64_t)base ? __ldg(a.waits + R0 - 1) : 0u;  // the range's predecessor wait
+  uint32_t slot = 0, phase = 0, rslot = rg.nsl - 1;  // slot of piece k, its parity, slot to refill
+  for (int64_t k = 0; k < npieces; ++k) {
+    if (k + rg.nsl - 1 < npieces) {
+      // refill the slot consumed in the previous iteration (reads are complete:
+      // every lane passed the __syncwarp at the end of that piece)
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      issue(k + rg.nsl - 1, rslot);
+    }
+    rslot = slot;
+    mbar_wait(bars + 8u * slot, phase);
+    const int64_t vs = v0 + k * (int64_t)PV;
+    const uint32_t nv = (uint32_t)min((int64_t)PV, v1 - vs);
+    const uint32_t sl = ring + slot * (PV * 16u) + 16u * lane;
+    const int32_t pw0 = (int32_t)(4 * (vs - v0));
+    for (uint32_t j = 0; j < nv; j += 32u) {  // windows of 32 vectors, warp-uniform
+      const int32_t pw = pw0 + 4 * (int32_t)j;
+      if (pw >= lo_r && pw + 384 <= hi_r && j + 96u < nv) {  // four fast windows
+        const uint32_t sa = sl + 16u * j;
+        const uint4 x = lds_v4(sa), y = lds_v4(sa + 512u), z = lds_v4(sa + 1024u), u = lds_v4(sa + 1536u);
+        fast_window(x, carry);
+        fast_window(y, carry);
+        fast_window(z, carry);
+        fast_window(u, carry);
+        j += 96u;
+        continue;
+      }
+      if (pw >= lo_r && pw + 128 <= hi_r && j + 32u < nv) {  // two fast windows
+        const uint4 x = lds_v4(sl + 16u * j), y = lds_v4(sl + 16u * (j + 32u));
+        fast_window(x, carry);
+        fast_window(y, carry);
+        j += 32u;
+        continue;
+      }
+      if (pw >= lo_r && pw <= hi_r) {
+        fast_window(lds_v4(sl + 16u * j), carry);
+        continue;
+      }
+      // ---- element-wise window: boundaries, served heads, skipped queues, range end
+      const uint32_t vl = j + lane;
+      const int64_t v = vs + vl;
+      uint32_t xv[4] = {0u, 0u, 0u, 0u};
+      if (vl < nv) {
+        if (v < nfull) {
+          const uint4 x = lds_v4(sl + 16u * j);
+          xv[0] = x.x; xv[1] = x.y; xv[2] = x.z; xv[3] = x.w;
+        } else {  // the partial last vector: its waits below `end` straight from global
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            const int64_t p = pv0 + 4 * v + i;
+            if (p >= (int64_t)base && p < (int64_t)end) xv[i] = __ldg(a.waits + p);
+          }
+        }
+      }
+      uint32_t prev = __shfl_up_sync(FULL, xv[3], 1);
+      if (lane == 0) prev = carry;
+      carry = __shfl_sync(FULL, xv[3], 31);
+      const int32_t pl = pw + 4 * lane;
+      const int32_t wend = min(pw + 128, (int32_t)(4 * (v1 - v0)));
+      // one SLO: G of every wait once; several SLOs: per queue pass (its snapshot's tables)
+      uint32_t gv[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) gv[i] = ONE ? G1(xv[i]) : 0u;
+      for (;;) {
+        if (!skip) {
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            const int32_t p = pl + i;
+            if (p >= qs_r && p < qe_r && vl < nv) {
+              tot += ONE ? gv[i] : Gg(xv[i]);
+              if (p > qs_r && xv[i] > (i ? xv[i - 1] : prev)) bad = 1u;
+            }
+          }
+        }
+        if (qe_r >= wend) break;  // the current queue reaches past this window
+        advance();
+      }
+    }
+    __syncwarp();
+    if (++slot == rg.nsl) {
+      slot = 0;
+      phase ^= 1u;
+    }
+  }
+  flush_snap();
 }
 
 // clip path (some head wait is within max L of x_c): (K_m, U_m) for every candidate
@@ -390,7 +701,7 @@ __global__ void __launch_bounds__(256) k1s_finish(const uint8_t *__restrict__ gi
       const CfgRec &C = cfg[k];
       uint64_t u, kk = 0;
       if (!(flags & F_SLOW)) {
-        u = acc[0] - acc[2 + m];
+        u = acc[0] - r.srv;  // fast path: U_m = total G - own served head (k1s_prep)
       } else {
         u = acc[2 + m];
         const uint32_t cB = r.c < r.B ? r.c : r.B;
@@ -464,6 +775,58 @@ cudaError_t launch_persistent(Kern kern, const uint8_t *img, const ImgLayout &la
   return cudaLaunchKernelEx(&cfg, kern, img, lay, a);
 }
 
+// fast-path launcher: the TMA ring kernel (default) or the register-pipelined
+// one (ES_K1_FAST=regs, or when the profile image leaves no room for 2 slots)
+template <int NW>
+cudaError_t launch_tma(const uint8_t *img, const ImgLayout &lay, const StreamArgs &a, int64_t nq, cudaStream_t st,
+                       int sms, int optin, bool regs) {
+  TmaRing rg{};
+  rg.ring_off = (lay.bytes + 127u) & ~127u;
+  const int64_t room = (int64_t)optin - 64 - rg.ring_off;
+  for (uint32_t pv = PV_MAX; pv >= 128u && rg.nsl < 3u; pv >>= 1) {
+    const int64_t per_slot = NW * (pv * 16 + 8);
+    rg.pv = pv;
+    rg.nsl = room > 0 ? (uint32_t)(room / per_slot < 6 ? room / per_slot : 6) : 0u;
+  }
+  if (regs || rg.nsl < 2) return launch_persistent(k1s_stream_fast, img, lay, a, nq, 8, lay.bytes, st, sms);
+  rg.mbar_off = rg.ring_off + NW * rg.nsl * rg.pv * 16u;
+  const size_t dyn = rg.mbar_off + NW * rg.nsl * 8u;
+  // single SLO: table bases as parameters; the masked A index must stay inside dynamic smem
+  const bool one = lay.ncfg == 1 && (size_t)lay.c0_offA + lay.c0_amask + 4u <= dyn;
+  auto kern = one ? k1s_stream_tma<true, NW> : k1s_stream_tma<false, NW>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
+  if (e != cudaSuccess) return e;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)sms);
+  cfg.blockDim = dim3(NW * 32);
+  cfg.dynamicSmemBytes = dyn;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, img, lay, a, rg);
+}
+
+// fast-path launcher: the TMA ring kernel (default; ES_K1_NW = consumer warps
+// per CTA) or the register-pipelined one (ES_K1_FAST=regs, or when the profile
+// image leaves no room for 2 slots per warp)
+cudaError_t launch_fast(const uint8_t *img, const ImgLayout &lay, const StreamArgs &a, int64_t nq, cudaStream_t st,
+                        int sms) {
+  const char *env = getenv("ES_K1_FAST");
+  const bool regs = env && strcmp(env, "regs") == 0;
+  int dev = 0, optin = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e == cudaSuccess) e = cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+  if (e != cudaSuccess) return e;
+  const char *nw = getenv("ES_K1_NW");
+  const int w = nw ? atoi(nw) : 16;
+  if (w == 32) return launch_tma<32>(img, lay, a, nq, st, sms, optin, regs);
+  if (w == 24) return launch_tma<24>(img, lay, a, nq, st, sms, optin, regs);
+  return launch_tma<16>(img, lay, a, nq, st, sms, optin, regs);
+}
+
 }  // namespace
 
 cudaError_t launch_score_stream(const uint8_t *img, const ImgLayout &lay, const es_snapshots &sn,
@@ -495,7 +858,7 @@ cudaError_t launch_score_stream(const uint8_t *img, const ImgLayout &lay, const 
   a.rec = reinterpret_cast<QRec *>(sp + acc_bytes + list_bytes);
   e = cudaMemsetAsync(a.acc, 0, acc_bytes, st);
   if (e == cudaSuccess) e = launch_persistent(k1s_prep, img, lay, a, nq, 256, lay.bytes, st, sms, false);
-  if (e == cudaSuccess) e = launch_persistent(k1s_stream_fast, img, lay, a, nq, 8, lay.bytes, st, sms);
+  if (e == cudaSuccess) e = launch_fast(img, lay, a, nq, st, sms);
   if (e == cudaSuccess) {
     if (lay.M <= 2) e = launch_persistent(k1s_stream_slow<2>, img, lay, a, nq, 8, lay.bytes, st, sms);
     else if (lay.M <= 4) e = launch_persistent(k1s_stream_slow<4>, img, lay, a, nq, 8, lay.bytes, st, sms);

@@ -416,3 +416,41 @@ def test_k1_all_mappings(monkeypatch, mode):
     test_k1_deep_snapshots(4, 300)
     test_k1_masks_and_flags()
     test_k1_harvested_snapshots()
+
+
+def test_k1_full_size_bench_batch():
+    """K1 at the bench's full size and launch configuration (bench.k1_batch:
+    65,536 5-C snapshots, 4.3 GB of waits, the TMA stream mapping): 512
+    sampled snapshots spread over every tile against the oracle, element by
+    element, plus properties that hold for every snapshot (Eq. 7's choice is
+    the argmin of the candidate scores, Q3 tie-break)."""
+    import bench
+    q_off, w0, tiles = bench.k1_batch(0)
+    M = 8
+    n = (q_off.size - 1) // M
+    prof = inputs.synth_profile(8, 5, list(range(1, 33)))
+    cfgs = [inputs.SchedCfg(tau=50000, b_max=32)]
+    h = es.es_load_profile(prof, cfgs)
+    o = es.es_score_candidates(h, to_dev(q_off, torch.uint64), to_dev(w0, torch.uint32).repeat(tiles))
+    torch.cuda.synchronize()
+    g = {k: np_of(v) for k, v in o.items()}
+    # sampled snapshots: their queues re-packed into a small CSR for the oracle
+    rng = np.random.default_rng(3)
+    ids = np.sort(rng.choice(n, 512, replace=False))
+    n0 = n // tiles
+    sub_off, parts = [0], []
+    for s in ids:
+        s0 = s % n0  # tile copies share the seeded waits of snapshot s0
+        for m in range(M):
+            lo, hi = int(q_off[s0 * M + m]), int(q_off[s0 * M + m + 1])
+            parts.append(w0[lo:hi])
+            sub_off.append(sub_off[-1] + hi - lo)
+    ref = oracle.decide_batch(prof, cfgs, np.array(sub_off, np.uint64), np.concatenate(parts))
+    sub = {k: g[k][ids] for k in ["m", "e", "B", "L", "S", "flags"]}
+    sub["cand"] = g["cand"].reshape(-1, M)[ids]
+    assert_k1_equal(sub, ref, M)
+    # every snapshot: the chosen model is the (S, m) argmin of its candidate scores
+    cand = g["cand"].reshape(-1, M)
+    ok = g["flags"] & 6 == 0
+    assert np.array_equal(np.argmin(cand[ok], axis=1), g["m"][ok].astype(np.int64))
+    assert np.array_equal(cand[ok].min(axis=1), g["S"][ok])
