@@ -39,7 +39,8 @@ def parse():
     ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--workload", default="cfg2")
+    ap.add_argument("--workload", default="cfg2", choices=sorted(PER_GPU))
+    ap.add_argument("--scenarios", type=int, default=0, help="scenarios per GPU (default: PER_GPU[workload])")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-k1", action="store_true", help="skip the K1 snapshot-scoring measurement")
@@ -54,11 +55,31 @@ def dist_env():
     return rank, world, local
 
 
-def rank_workload(name, rank):
+# per-GPU scenario counts (weak scaling) and descriptions of the BASELINE.json
+# configs; cfg4 is the 1M-scenario sweep sharded over 8 GPUs, the two config-5
+# readings run host-generated shards of 262,144 scenarios
+PER_GPU = {"cfg1": 1, "cfg2": 4096, "cfg3": 65536, "cfg4": 131072, "cfg5a": 1024, "cfg5b": 16384}
+DESC = {
+    "cfg1": "cfg1 (BASELINE configs[0]): 1 scenario x 3 DNNs x 3 exits x batch {1,2,4,8}, 1,000-request Poisson trace, "
+            "tau 50 ms",
+    "cfg2": "cfg2 (BASELINE configs[1]): 4,096 scenarios/GPU x 4 DNNs x 4 exits x batch 1-16, 10k-request Poisson "
+            "traces, rho 0.60-1.20, tau 50 ms",
+    "cfg3": "cfg3 (BASELINE configs[2]): 65,536 scenarios/GPU x 8 DNNs x 5 exits x batch 1-32, 10k-request bursty "
+            "MMPP traces, tau 20-100 ms x rho 0.60-1.20 (117 groups)",
+    "cfg4": "cfg4 (BASELINE configs[3]): 1M-scenario SLO x rate sweep, 131,072 scenarios/GPU (1/8 shard) x 4 DNNs x "
+            "4 exits x batch 1-16, 10k-request Poisson traces, 16 tau x 16 rho groups",
+    "cfg5a": "cfg5-A (BASELINE configs[4], long-trace reading): 8 DNNs x 5 exits x batch 1-32, 1M-request Poisson "
+             "traces at rho_full 1.5, 1,024-scenario shard/GPU",
+    "cfg5b": "cfg5-B (BASELINE configs[4], deep-queue reading): 8 DNNs x 5 exits x batch 1-32, 50k-request traces at "
+             "rho_shallow 1.5 (queues up to ~4k), 16,384-scenario shard/GPU",
+}
+
+
+def rank_workload(name, rank, S=None):
     """Weak scaling: rank r replays scenarios [r*S, (r+1)*S) of the config's
     scenario sequence (same generator, same shapes, distinct seeds)."""
     import inputs
-    S = inputs.total_scenarios(name)
+    S = S or PER_GPU.get(name, inputs.total_scenarios(name))
     ids = np.arange(rank * S, (rank + 1) * S, dtype=np.int64)
     return inputs.workload(name, scen_ids=ids), S
 
@@ -210,11 +231,11 @@ def run_reference(args, rank, world):
     if rank != 0:
         return
     import oracle
-    w, S = rank_workload(args.workload, 0)
-    tr = w.traces
-    cores = os.cpu_count() or 1
-    chunk = 512
     import inputs
+    S = args.scenarios or PER_GPU[args.workload]
+    cores = os.cpu_count() or 1
+    per = inputs.workload(args.workload, scen_ids=np.arange(1)).traces.arrival.size  # requests per scenario
+    chunk = int(max(1, min(512, S, 5e6 // per)))
     nsteps = args.warmup + args.steps
     times = []
     dec = 0
@@ -223,18 +244,18 @@ def run_reference(args, rank, world):
         ids = np.arange(lo, lo + chunk)
         sub = inputs.workload(args.workload, scen_ids=ids)
         t0 = time.perf_counter()
-        o = oracle.replay_batch(w.profile, w.cfgs, sub.traces, full=False, nthreads=cores)
+        o = oracle.replay_batch(sub.profile, sub.cfgs, sub.traces, full=False, nthreads=cores)
         dt = time.perf_counter() - t0
         if k >= args.warmup:
             times.append(dt)
             dec += int(o["stats"][:, 0].sum())
     tot = sum(times)
     v = dec / tot
-    sample = f"{chunk} scenarios of {args.workload} per step (cycling through the {S}-scenario batch), full 10k-request traces"
+    sample = f"{chunk} scenarios of {args.workload} per step (cycling through the {S}-scenario batch), full traces"
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": 1e3 * tot / args.steps, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "u32", "data": "synthetic",
-            "config": {"workload": f"{args.workload} (BASELINE configs[1])", "scenarios_per_step": chunk},
+            "config": {"workload": DESC[args.workload], "scenarios_per_step": chunk},
             "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": sample},
             "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
@@ -260,7 +281,7 @@ def main():
         pg = dist.group.WORLD
     import inputs
 
-    w, S = rank_workload(args.workload, rank)
+    w, S = rank_workload(args.workload, rank, args.scenarios)
     G = inputs.n_groups(args.workload)
     h = es.es_load_profile(w.profile, w.cfgs, device=local)
     dtr = engine.upload_traces(w.traces, dev)
@@ -350,10 +371,9 @@ def main():
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "u32", "data": "synthetic",
-            "config": {"workload": f"{args.workload} (BASELINE configs[1]): 4,096 scenarios/GPU x 4 DNNs x 4 exits "
-                                   f"x batch 1-16, 10k-request Poisson traces, rho 0.60-1.20, tau 50 ms",
-                       "scenarios_per_gpu": S, "requests_per_gpu": total, "groups": G,
-                       "l2": "inputs larger than L2 (164 MB arrivals/GPU > 126 MB)",
+            "config": {"workload": DESC[args.workload], "scenarios_per_gpu": S, "requests_per_gpu": total, "groups": G,
+                       "l2": f"inputs larger than L2 ({4 * total / 1e6:.0f} MB arrivals/GPU > 126 MB)"
+                             if 4 * total > 126e6 else f"inputs fit L2 ({4 * total / 1e6:.1f} MB arrivals/GPU)",
                        "parallelism": f"scenario-sharded x{world}, NCCL all_reduce of group histograms"},
             "scored_candidates_per_s": cand_all * args.steps / (ms_max / 1e3),
             "decisions_per_step": dec_all, "gpu_launches": launches, "roofline": roof}
@@ -400,21 +420,25 @@ def main():
     if rank == 0 and world == 1 and not args.no_cpu_baseline and not args.ncu:
         import oracle
         cores = os.cpu_count() or 1
+        # bounded sample: the first k scenarios of the batch, <= ~50M requests
+        per = total / S
+        k = S if total <= 50e6 else max(1, int(50e6 // per))
+        ws = w if k == S else inputs.workload(args.workload, scen_ids=np.arange(k, dtype=np.int64))
         reps = 0
         t = time.perf_counter()
         while True:  # >= ~1 s wall (~16 s of CPU work on 16 cores)
-            o = oracle.replay_batch(w.profile, w.cfgs, w.traces, full=False, nthreads=cores)
+            o = oracle.replay_batch(ws.profile, ws.cfgs, ws.traces, full=False, nthreads=cores)
             reps += 1
             if time.perf_counter() - t > 1.0:
                 break
         dt = (time.perf_counter() - t) / reps
-        assert np.array_equal(o["stats"], st), "oracle and GPU disagree on the bench batch"
-        assert np.array_equal(o["p95"], out["p95"].cpu().numpy())
+        assert np.array_equal(o["stats"], st[:k]), "oracle and GPU disagree on the bench batch"
+        assert np.array_equal(o["p95"], out["p95"].cpu().numpy()[:k])
+        what = f"the full {S}-scenario bench batch" if k == S else f"the first {k} of the {S} bench scenarios"
         line["cpu_baseline"] = {"value": int(o["stats"][:, 0].sum()) / dt, "unit": UNIT, "cores": cores,
                                 "kind": "oracle",
-                                "sample": f"the full {S}-scenario bench batch (rank 0), {reps} replay(s), "
-                                          f"{dt:.2f} s wall each on {cores} threads",
-                                "parity": "bit-exact on all per-scenario counters and P95 of the batch"}
+                                "sample": f"{what} (rank 0), {reps} replay(s), {dt:.2f} s wall each on {cores} threads",
+                                "parity": f"bit-exact on all per-scenario counters and P95 of those {k} scenarios"}
     if rank == 0:
         print(json.dumps(line), flush=True)
     if world > 1:
