@@ -90,10 +90,31 @@ typedef struct {
   uint32_t clip_C;  /* clip constant C of Eq. 3, 1..15 (C = 10)           */
   uint32_t b_max;   /* B_max of Eq. 5, 1 <= b_max <= bs[nb-1]                    */
   uint32_t warmup;  /* completions dropped from the statistics (100)      */
-  uint32_t policy;  /* ES_POLICY_EDGESERVING (only value in this version)        */
+  uint32_t policy;  /* selection rule, ES_POLICY_* below (Algorithm 1 = 0)          */
 } es_sched_cfg;
 
+/*
+ * Selection policies.  EDGESERVING is Algorithm 1.  The others
+ * are the paper's baselines (§VI-A) and core-design ablations
+ * (§VI-H), read as DESIGN.md Q26; they reuse a1-a5 and a8-a10:
+ *   ALL_FINAL    longest queue first (LQF; ties lowest m), B* of Eq. 5, deepest allowed exit
+ *   ALL_EARLY    LQF, B* of Eq. 5, shallowest allowed exit
+ *   EE_LQF       LQF, then Eq. 5 / Eq. 6 for the chosen queue
+ *   EE_EDF       least slack tau - w_head (largest head wait; ties lowest m), Eq. 5 / Eq. 6
+ *   ALLFINAL_DA  Eq. 7 stability-score selection with every candidate at its deepest exit
+ *   OURS_BS1     Algorithm 1 with B* = 1
+ * A fixed exit is feasible iff w_head + L <= tau.  LQF / EDF policies score
+ * nothing: the decision's S is 0.  Replay (es_replay_traces) accepts every
+ * policy; es_score_candidates (K1) scores EdgeServing only (ES_ERR_ARG).
+ */
 #define ES_POLICY_EDGESERVING 0u
+#define ES_POLICY_ALL_FINAL 1u
+#define ES_POLICY_ALL_EARLY 2u
+#define ES_POLICY_EE_LQF 3u
+#define ES_POLICY_EE_EDF 4u
+#define ES_POLICY_ALLFINAL_DA 5u
+#define ES_POLICY_OURS_BS1 6u
+#define ES_POLICY_COUNT 7u
 
 /*
  * Validate the profile (complete grid; L > 0; non-decreasing in batch;

@@ -140,6 +140,7 @@ class SchedCfg:
     b_max: int
     C: int = 10
     warmup: int = 100
+    policy: int = 0  # selection rule id (C ABI ES_POLICY_*): 0 = EdgeServing, 1..6 = paper baselines/ablations
 
 
 @dataclass

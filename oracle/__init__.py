@@ -109,12 +109,18 @@ def validate_profile(prof):
     return int(st), tuple(int(x) for x in bad)
 
 
+# selection policies (oracle.c OR_POL_*, Q26)
+POLICIES = {"edgeserving": 0, "all_final": 1, "all_early": 2, "ee_lqf": 3, "ee_edf": 4, "allfinal_da": 5,
+            "ours_bs1": 6}
+
+
 def _cfg_arrays(cfgs):
     tau = np.array([c.tau for c in cfgs], np.uint32)
     C = np.array([c.C for c in cfgs], np.uint32)
     bm = np.array([c.b_max for c in cfgs], np.uint32)
     wu = np.array([c.warmup for c in cfgs], np.uint32)
-    return tau, C, bm, wu
+    pol = np.array([getattr(c, "policy", 0) for c in cfgs], np.uint32)
+    return tau, C, bm, wu, pol
 
 
 def decide_batch(prof, cfgs, q_off, waits, cfg_idx=None):
@@ -123,7 +129,7 @@ def decide_batch(prof, cfgs, q_off, waits, cfg_idx=None):
     q_off = np.ascontiguousarray(q_off, np.uint64)
     waits = np.ascontiguousarray(waits, np.uint32)
     n = (q_off.size - 1) // M
-    tau, C, bm, _ = _cfg_arrays(cfgs)
+    tau, C, bm, _, pol = _cfg_arrays(cfgs)
     ci = None if cfg_idx is None else np.ascontiguousarray(cfg_idx, np.uint16)
     out = {"m": np.zeros(n, np.uint8), "e": np.zeros(n, np.uint8), "B": np.zeros(n, np.uint16),
            "L": np.zeros(n, np.uint32), "S": np.zeros(n, np.uint64), "flags": np.zeros(n, np.uint8),
@@ -132,7 +138,7 @@ def decide_batch(prof, cfgs, q_off, waits, cfg_idx=None):
     lat = np.ascontiguousarray(prof.lat, np.uint32)
     mask = np.ascontiguousarray(prof.mask, np.uint8)
     st = lib().or_decide_batch(
-        M, prof.E, prof.nb, _p(bs), _p(lat), _p(mask), _p(tau), _p(C), _p(bm), len(cfgs),
+        M, prof.E, prof.nb, _p(bs), _p(lat), _p(mask), _p(tau), _p(C), _p(bm), _p(pol), len(cfgs),
         ctypes.c_int64(n), _p(ci), _p(q_off), _p(waits), _p(out["m"]), _p(out["e"]), _p(out["B"]),
         _p(out["L"]), _p(out["S"]), _p(out["flags"]), _p(out["cand"]), _p(out["cand_dbl"]))
     if st:
@@ -147,7 +153,7 @@ def replay_batch(prof, cfgs, traces, full=True, dec_cap=0, nthreads=1):
     M = prof.M
     n = traces.n_scen
     total = int(traces.arr_off[-1])
-    tau, C, bm, wu = _cfg_arrays(cfgs)
+    tau, C, bm, wu, pol = _cfg_arrays(cfgs)
     arr_off = np.ascontiguousarray(traces.arr_off, np.uint64)
     arrival = np.ascontiguousarray(traces.arrival, np.uint32)
     ci = np.ascontiguousarray(traces.cfg_idx, np.uint16)
@@ -169,7 +175,7 @@ def replay_batch(prof, cfgs, traces, full=True, dec_cap=0, nthreads=1):
     mask = np.ascontiguousarray(prof.mask, np.uint8)
     g = out.get
     st = lib().or_replay_batch(
-        M, prof.E, prof.nb, _p(bs), _p(lat), _p(mask), _p(tau), _p(C), _p(bm), _p(wu), len(cfgs),
+        M, prof.E, prof.nb, _p(bs), _p(lat), _p(mask), _p(tau), _p(C), _p(bm), _p(wu), _p(pol), len(cfgs),
         ctypes.c_int64(n), _p(ci), _p(arr_off), _p(arrival), _p(g("completion")), _p(g("exit")),
         _p(g("lat")), _p(out["stats"]), _p(out["p95"]), ctypes.c_int64(dec_cap), _p(g("dec_t")),
         _p(g("dec_m")), _p(g("dec_e")), _p(g("dec_B")), _p(g("dec_L")), _p(g("dec_S")),

@@ -136,3 +136,51 @@ def tree_min_violations(arrivals, prof, tau, b_max):
     _tree([list(map(int, a)) for a in arrivals], t0, [0] * len(arrivals), prof, tau, b_max, bs, 0,
           best, None)
     return best[0]
+
+
+# the paper's baselines (§VI-A) and ablations (§VI-H),
+# read as DESIGN.md Q26; names as in SPEC's policy_decide
+POLICY_IDS = {"edgeserving": 0, "all_final": 1, "all_early": 2, "ee_lqf": 3, "ee_edf": 4, "allfinal_da": 5,
+              "ours_bs1": 6}
+
+
+def literal_policy_decide(prof, tau, C, b_max, waits, policy):
+    """One decision of `policy` on head-first waits, float64 scores.  Returns
+    (m*, e*, B*, feasible, scores) with scores = {m: S} for the scoring
+    policies ({} otherwise), or None when every queue is empty."""
+    bs = [int(b) for b in prof.bs]
+    nonempty = [m for m, q in enumerate(waits) if q]
+    if not nonempty:
+        return None
+
+    def params(m):
+        q = waits[m]
+        B = 1 if policy == "ours_bs1" else batch_size(len(q), b_max, bs)  # "fixes batch size to 1"
+        bi = bs.index(B)
+        row = [int(prof.lat[m, e, bi]) for e in range(prof.E)]
+        allowed = [bool(x) for x in prof.mask[m]]
+        if policy in ("all_final", "allfinal_da"):  # "always executes them at the deepest exit"
+            e = max(i for i in range(prof.E) if allowed[i])
+            feas = q[0] + row[e] <= tau
+        elif policy == "all_early":  # "always executes them at the shallowest exit"
+            e = min(i for i in range(prof.E) if allowed[i])
+            feas = q[0] + row[e] <= tau
+        else:  # profile-based exit selection, Eq. 6
+            e, feas = exit_point(row, allowed, q[0], tau)
+        return e, B, feas, row[e]
+
+    if policy in ("all_final", "all_early", "ee_lqf"):  # longest queue first
+        m_star = min(nonempty, key=lambda m: (-len(waits[m]), m))
+        e, B, feas, _ = params(m_star)
+        return m_star, e, B, feas, {}
+    if policy == "ee_edf":  # least remaining SLO slack tau - w of the oldest task
+        m_star = min(nonempty, key=lambda m: (tau - waits[m][0], m))
+        e, B, feas, _ = params(m_star)
+        return m_star, e, B, feas, {}
+    scores = {}
+    for m in nonempty:
+        e, B, feas, L = params(m)
+        scores[m] = stability_score(predict(waits, m, B, L), tau, C)
+    m_star = min(scores, key=lambda m: (scores[m], m))
+    e, B, feas, _ = params(m_star)
+    return m_star, e, B, feas, scores

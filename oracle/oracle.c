@@ -44,6 +44,22 @@
 /* status codes (numbers mirror nothing; the Python side maps them) */
 enum { OR_OK = 0, OR_ERR_ARG = 1, OR_ERR_PROFILE = 2, OR_ERR_RANGE = 3, OR_ERR_UNSORTED = 4 };
 
+/*
+ * Selection policies (numbering = the C ABI's ES_POLICY_*).  EDGESERVING is
+ * Algorithm 1.  The others are the paper's baselines (§VI-A) and
+ * core-design ablations (§VI-H), with DESIGN.md reading Q26:
+ *   ALL_FINAL    longest queue first (LQF), B from Eq. 5, deepest allowed exit
+ *   ALL_EARLY    LQF, B from Eq. 5, shallowest allowed exit
+ *   EE_LQF       LQF, then Eq. 5 / Eq. 6 for the chosen queue
+ *   EE_EDF       least remaining slack tau - w_head (= largest head wait), Eq. 5 / 6
+ *   ALLFINAL_DA  Eq. 7 stability-score selection, every candidate at its deepest exit
+ *   OURS_BS1     Algorithm 1 with the batch fixed to 1 (bs[0])
+ * LQF / EDF ties go to the lowest model index; those four policies score
+ * nothing (S = 0).  A fixed exit is feasible iff w_head + L <= tau.
+ */
+enum { OR_POL_EDGESERVING = 0, OR_POL_ALL_FINAL = 1, OR_POL_ALL_EARLY = 2, OR_POL_EE_LQF = 3,
+       OR_POL_EE_EDF = 4, OR_POL_ALLFINAL_DA = 5, OR_POL_OURS_BS1 = 6, OR_POL_N = 7 };
+
 /* ------------------------------------------------------------------ tables */
 
 /* distance of a real value to the nearest integer */
@@ -115,6 +131,7 @@ typedef struct {
   const uint8_t *mask;  /* [M][E] allowed exits, nonzero = allowed */
   /* scheduler config */
   uint32_t tau, C, b_max, warmup;
+  uint32_t policy; /* OR_POL_*: Algorithm 1 or one of the paper's baselines / ablations */
   /* derived tables (Q5) */
   uint64_t x_c, C_q;
   uint32_t r;
@@ -166,14 +183,15 @@ int or_validate_profile(int M, int E, int nb, const int32_t *bs, const uint32_t 
 
 static int ctx_init(or_ctx *c, int M, int E, int nb, const int32_t *bs, const uint32_t *lat,
                     const uint8_t *mask, uint32_t tau, uint32_t C, uint32_t b_max,
-                    uint32_t warmup) {
+                    uint32_t warmup, uint32_t policy) {
   memset(c, 0, sizeof(*c));
   int32_t bad[3];
   int st = or_validate_profile(M, E, nb, bs, lat, mask, bad);
   if (st) return st;
   if (b_max < 1u || b_max > (uint32_t)bs[nb - 1]) return OR_ERR_ARG;
+  if (policy >= OR_POL_N) return OR_ERR_ARG;
   c->M = M; c->E = E; c->nb = nb; c->bs = bs; c->lat = lat; c->mask = mask;
-  c->tau = tau; c->C = C; c->b_max = b_max; c->warmup = warmup;
+  c->tau = tau; c->C = C; c->b_max = b_max; c->warmup = warmup; c->policy = policy;
   int cap = (int)((((uint64_t)tau * 4u) >> OR_SBITS) + 4);
   c->A = (uint32_t *)malloc(sizeof(uint32_t) * (size_t)cap);
   double mg;
@@ -235,13 +253,42 @@ typedef struct {
   double S_dbl;
 } or_cand;
 
+static int deepest_allowed(const or_ctx *c, int m) {
+  for (int e = c->E - 1; e >= 0; --e)
+    if (allowed(c, m, e)) return e;
+  return 0;
+}
+
+static int shallowest_allowed(const or_ctx *c, int m) {
+  for (int e = 0; e < c->E; ++e)
+    if (allowed(c, m, e)) return e;
+  return 0;
+}
+
+static int uses_score(const or_ctx *c) {
+  return c->policy == OR_POL_EDGESERVING || c->policy == OR_POL_ALLFINAL_DA || c->policy == OR_POL_OURS_BS1;
+}
+
+/* a3 + a4 of candidate m under the cfg's policy: batch (Eq. 5, or 1 for
+   OURS_BS1) and exit (Eq. 6, or the policy's fixed exit) */
+static void cand_params(const or_ctx *c, int m, uint64_t len, uint64_t w_max, or_cand *out) {
+  int bi = c->policy == OR_POL_OURS_BS1 ? 0 : batch_index(c, len);
+  int e, feasible;
+  if (c->policy == OR_POL_ALL_FINAL || c->policy == OR_POL_ALLFINAL_DA || c->policy == OR_POL_ALL_EARLY) {
+    e = c->policy == OR_POL_ALL_EARLY ? shallowest_allowed(c, m) : deepest_allowed(c, m);
+    feasible = w_max + LAT(c, m, e, bi) <= c->tau;
+  } else {
+    e = exit_select(c, m, bi, w_max, &feasible);
+  }
+  out->e = e; out->B = c->bs[bi]; out->bi = bi; out->feasible = feasible; out->L = LAT(c, m, e, bi);
+  out->S_q = 0; out->S_dbl = 0.0;
+}
+
 static void score_candidate(const or_ctx *c, int m, const uint64_t *len,
                             const uint32_t *const *waits, or_cand *out) {
-  int bi = batch_index(c, len[m]);
-  int B = c->bs[bi];
-  int feasible;
-  int e = exit_select(c, m, bi, waits[m][0], &feasible);
-  uint32_t L = LAT(c, m, e, bi);
+  cand_params(c, m, len[m], waits[m][0], out);
+  int bi = out->bi, B = out->B, e = out->e;
+  uint32_t L = out->L;
   uint64_t K = 0;
   unsigned __int128 U = 0;
   double S_dbl = 0.0;
@@ -261,25 +308,37 @@ static void score_candidate(const or_ctx *c, int m, const uint64_t *len,
     unsigned __int128 HU = (unsigned __int128)c->H[((size_t)m * c->E + e) * c->nb + bi] * U;
     S += (uint64_t)(HU >> OR_F);
   }
-  out->e = e; out->B = B; out->bi = bi; out->feasible = feasible; out->L = L;
   out->S_q = S; out->S_dbl = S_dbl;
 }
 
 /*
  * decide() on one snapshot (Algorithm 1; Eq. 7 argmin with
- * tie-break lowest model index, Q3).  Returns the chosen model or -1 when
- * every queue is empty (no-work signal).
+ * tie-break lowest model index, Q3; or the cfg's baseline policy, Q26).
+ * Returns the chosen model or -1 when every queue is empty (no-work signal,
+ * S:233).  *n_cand = non-empty queues.
  */
 static int decide(const or_ctx *c, const uint64_t *len, const uint32_t *const *waits,
                   or_cand *cands /* [M] */, int *n_cand) {
   int best = -1;
   *n_cand = 0;
+  if (uses_score(c)) {
+    for (int m = 0; m < c->M; ++m) {
+      if (len[m] == 0) continue;
+      score_candidate(c, m, len, waits, &cands[m]);
+      (*n_cand)++;
+      if (best < 0 || cands[m].S_q < cands[best].S_q) best = m;
+    }
+    return best;
+  }
+  /* LQF: most queued tasks; EDF: least slack tau - w_head, i.e. the largest
+     head wait; strict > keeps the lowest model index on ties */
   for (int m = 0; m < c->M; ++m) {
     if (len[m] == 0) continue;
-    score_candidate(c, m, len, waits, &cands[m]);
     (*n_cand)++;
-    if (best < 0 || cands[m].S_q < cands[best].S_q) best = m;
+    if (best < 0) { best = m; continue; }
+    if (c->policy == OR_POL_EE_EDF ? waits[m][0] > waits[best][0] : len[m] > len[best]) best = m;
   }
+  if (best >= 0) cand_params(c, best, len[best], waits[best][0], &cands[best]);
   return best;
 }
 
@@ -291,13 +350,14 @@ static int decide(const or_ctx *c, const uint64_t *len, const uint32_t *const *w
  */
 int or_decide_batch(int M, int E, int nb, const int32_t *bs, const uint32_t *lat,
                     const uint8_t *mask, const uint32_t *tau, const uint32_t *C,
-                    const uint32_t *b_max, int ncfg, int64_t n, const uint16_t *cfg_idx,
+                    const uint32_t *b_max, const uint32_t *policy, int ncfg, int64_t n,
+                    const uint16_t *cfg_idx,
                     const uint64_t *q_off, const uint32_t *waits, uint8_t *o_m, uint8_t *o_e,
                     uint16_t *o_B, uint32_t *o_L, uint64_t *o_S, uint8_t *o_flags,
                     uint64_t *o_cand, double *o_cand_dbl) {
   or_ctx *ctx = (or_ctx *)calloc((size_t)ncfg, sizeof(or_ctx));
   for (int k = 0; k < ncfg; ++k) {
-    int st = ctx_init(&ctx[k], M, E, nb, bs, lat, mask, tau[k], C[k], b_max[k], 0);
+    int st = ctx_init(&ctx[k], M, E, nb, bs, lat, mask, tau[k], C[k], b_max[k], 0, policy ? policy[k] : 0u);
     if (st) {
       for (int j = 0; j < k; ++j) ctx_free(&ctx[j]);
       free(ctx);
@@ -335,7 +395,7 @@ int or_decide_batch(int M, int E, int nb, const int32_t *bs, const uint32_t *lat
     o_S[s] = cands[best].S_q;
     o_flags[s] = (uint8_t)(cands[best].feasible ? 1 : 0);
     for (int m = 0; m < M; ++m)
-      if (len[m]) {
+      if (len[m] && uses_score(c)) { /* LQF / EDF policies score nothing */
         if (o_cand) o_cand[s * M + m] = cands[m].S_q;
         if (o_cand_dbl) o_cand_dbl[s * M + m] = cands[m].S_dbl;
       }
@@ -442,7 +502,7 @@ static int replay_one(const or_ctx *c, const uint64_t *n, const uint32_t *const 
     for (int m = 0; m < M; ++m)
       for (uint64_t i = 0; i < len[m]; ++i) live += (uint64_t)wbuf[m][i] < c->x_c;
     stats[ST_LIVE] += live;
-    stats[ST_TERMS] += live * (uint64_t)nc;
+    if (uses_score(c)) stats[ST_TERMS] += live * (uint64_t)nc; /* Eq. 4 terms: scoring policies only */
     for (int m = 0; m < M; ++m)
       if (len[m]) stats[ST_CELLS] += (uint64_t)n_allowed(c, m);
     if (!d->feasible) stats[ST_INFEASIBLE]++;
@@ -537,7 +597,8 @@ static void *replay_worker(void *arg) {
  */
 int or_replay_batch(int M, int E, int nb, const int32_t *bs, const uint32_t *lat,
                     const uint8_t *mask, const uint32_t *tau, const uint32_t *C,
-                    const uint32_t *b_max, const uint32_t *warmup, int ncfg, int64_t n_scen,
+                    const uint32_t *b_max, const uint32_t *warmup, const uint32_t *policy, int ncfg,
+                    int64_t n_scen,
                     const uint16_t *cfg_idx, const uint64_t *arr_off, const uint32_t *arrival,
                     uint32_t *completion, uint8_t *exit_used, uint32_t *lat_out,
                     uint64_t *stats, uint32_t *p95, int64_t dec_cap, uint32_t *dec_t,
@@ -545,7 +606,7 @@ int or_replay_batch(int M, int E, int nb, const int32_t *bs, const uint32_t *lat
                     uint64_t *dec_S, uint8_t *dec_f, int nthreads) {
   or_ctx *ctx = (or_ctx *)calloc((size_t)ncfg, sizeof(or_ctx));
   for (int k = 0; k < ncfg; ++k) {
-    int st = ctx_init(&ctx[k], M, E, nb, bs, lat, mask, tau[k], C[k], b_max[k], warmup[k]);
+    int st = ctx_init(&ctx[k], M, E, nb, bs, lat, mask, tau[k], C[k], b_max[k], warmup[k], policy ? policy[k] : 0u);
     if (st) {
       for (int q = 0; q < k; ++q) ctx_free(&ctx[q]);
       free(ctx);

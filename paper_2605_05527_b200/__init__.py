@@ -165,7 +165,7 @@ def es_load_profile(profile, cfgs, device=0) -> Profile:
                     None if mask is None else mask.ctypes.data)
     arr = (SchedCfg * len(cfgs))()
     for i, c in enumerate(cfgs):
-        arr[i] = SchedCfg(int(c.tau), int(c.C), int(c.b_max), int(c.warmup), 0)
+        arr[i] = SchedCfg(int(c.tau), int(c.C), int(c.b_max), int(c.warmup), int(getattr(c, "policy", 0)))
     h = ctypes.c_void_p()
     _check(lib().es_load_profile(ctypes.byref(d), arr, len(cfgs), int(device), ctypes.byref(h)))
     return Profile(h, int(profile.M), int(profile.E), int(bs.size), list(cfgs), int(device))

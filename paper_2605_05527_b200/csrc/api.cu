@@ -110,7 +110,7 @@ es_status validate_cfg(const es_profile_desc *d, const es_sched_cfg &c, int k) {
   if (c.b_max > (uint32_t)d->batch_sizes[d->nb - 1])
     return fail(ES_ERR_OUT_OF_GRID, "cfg %d: b_max=%u above the largest profiled batch %d", k, c.b_max,
                 d->batch_sizes[d->nb - 1]);
-  if (c.policy != ES_POLICY_EDGESERVING) return fail(ES_ERR_ARG, "cfg %d: unknown policy %u", k, c.policy);
+  if (c.policy >= ES_POLICY_COUNT) return fail(ES_ERR_ARG, "cfg %d: unknown policy %u", k, c.policy);
   return ES_OK;
 }
 
@@ -164,6 +164,7 @@ es_status es_load_profile(const es_profile_desc *desc, const es_sched_cfg *cfgs,
     r.C = cfgs[k].clip_C;
     r.b_max = cfgs[k].b_max;
     r.warmup = cfgs[k].warmup;
+    r.policy = cfgs[k].policy;
     // capacity bound for A: x_c <= tau (1 + ln C) + 1 (+2 slack for rounding)
     const double xmax = std::floor((double)r.tau * (1.0 + std::log((double)r.C)) * (1.0 + 1e-12)) + 3.0;
     const uint32_t rr = (1024u - r.tau % 1024u) % 1024u;
@@ -179,6 +180,8 @@ es_status es_load_profile(const es_profile_desc *desc, const es_sched_cfg *cfgs,
     r.status = 0xFFFFFFFFu;
   }
   lay.bytes = off;
+  lay.pol_mask = 0;
+  for (int k = 0; k < ncfg; ++k) lay.pol_mask |= 1u << cfgs[k].policy;
   {
     uint32_t p2 = 1;
     while (p2 < recs[0].nA_cap) p2 <<= 1;
@@ -282,6 +285,10 @@ es_status es_score_candidates(const es_profile *p, const es_snapshots *sn, es_de
   if (sn->n == 0) return ES_OK;
   if (!sn->q_off || !sn->waits_us || !out->m || !out->e || !out->B || !out->L_us || !out->score_q || !out->flags)
     return fail(ES_ERR_ARG, "null snapshot input or decision output pointer");
+  for (size_t k = 0; k < p->cfgs.size(); ++k)
+    if (p->cfgs[k].policy != ES_POLICY_EDGESERVING)
+      return fail(ES_ERR_ARG, "es_score_candidates scores EdgeServing only (cfg %zu has policy %u)", k,
+                  p->cfgs[k].policy);
   DeviceGuard guard(p->device);
   CK(launch_score(p->d_img, p->lay, *sn, *out, p->d_status, (cudaStream_t)stream, p->sms), "k1_score");
   const_cast<es_profile *>(p)->launches++;
@@ -300,7 +307,9 @@ es_status es_replay_traces(const es_profile *p, const es_traces *tr, es_replay_o
   // K2 mapping: lane segments per scenario (k2_replay.cu, default) or
   // ES_K2=lane: one lane per model queue (k2_lane.cu; same integers)
   const char *k2 = getenv("ES_K2");
-  if (!(k2 && strcmp(k2, "lane") == 0)) {
+  bool any_policy = false;  // the lane mapping replays EdgeServing only
+  for (const es_sched_cfg &c : p->cfgs) any_policy |= c.policy != ES_POLICY_EDGESERVING;
+  if (!(k2 && strcmp(k2, "lane") == 0) || any_policy) {
     int nl = 0;
     CK(launch_replay(p->d_img, p->lay, *tr, *out, p->d_status, p->d_work, (cudaStream_t)stream, p->sms, &nl),
        "k2_replay");

@@ -38,8 +38,15 @@ struct SmemCfg {
   uint32_t off_A, off_Bt, off_H, off_bidx;  // byte offsets into the staged image
   uint32_t tau, b_max, warmup, x_c, r, nA1;
   uint32_t fast_lim;  // head waits below it cannot clip for any candidate
+  uint32_t policy;    // ES_POLICY_* (Q26)
   uint64_t C_q;
 };
+
+// policies that select by the stability score (Eq. 7) -- the others pick by
+// queue length (LQF) or head wait (EDF) and score nothing
+__device__ __forceinline__ bool policy_scores(uint32_t pol) {
+  return pol == ES_POLICY_EDGESERVING || pol == ES_POLICY_ALLFINAL_DA || pol == ES_POLICY_OURS_BS1;
+}
 
 struct SmemProf {
   const uint8_t *sm;
@@ -78,6 +85,7 @@ __device__ __forceinline__ SmemCfg smem_cfg(const SmemProf &p, int k) {
   s.r = c.r;
   s.nA1 = c.nA - 1u;
   s.fast_lim = c.fast_lim;
+  s.policy = c.policy;
   s.C_q = c.C_q;
   return s;
 }
@@ -249,7 +257,12 @@ __device__ __forceinline__ Cand cand_params(const Seg<LPS, MM> &sg, const SmemPr
                                             uint32_t len, uint32_t wmax) {
   constexpr int GL = Seg<LPS, MM>::GL;
   Cand k;
-  const uint32_t cap = len < C.b_max ? len : C.b_max;
+  // Eq. 5 (OURS_BS1: B* = bs[0] = 1); fixed exits for ALL_FINAL / ALLFINAL_DA
+  // (deepest allowed) and ALL_EARLY (shallowest allowed), else Eq. 6
+  const uint32_t cap = C.policy == ES_POLICY_OURS_BS1 ? 1u : (len < C.b_max ? len : C.b_max);
+  const int fixed = (C.policy == ES_POLICY_ALL_FINAL || C.policy == ES_POLICY_ALLFINAL_DA) ? 1
+                    : C.policy == ES_POLICY_ALL_EARLY                                    ? 2
+                                                                                         : 0;
   const int gg = sg.grp < P.M ? sg.grp : 0;
   const uint32_t bi = P.sm[C.off_bidx + cap];
   k.B = P.bs[bi];
@@ -264,9 +277,11 @@ __device__ __forceinline__ Cand cand_params(const Seg<LPS, MM> &sg, const SmemPr
     bits = sg.gbits(__ballot_sync(FULL, ok));
     k.feas = bits != 0u;
     k.e = k.feas ? 31u - __clz(bits) : (uint32_t)(__ffs(mbits) - 1);
+    if (fixed) k.e = fixed == 1 ? 31u - __clz(mbits) : (uint32_t)(__ffs(mbits) - 1);
     const int src = sg.grp * GL + (int)k.e;
     k.L = __shfl_sync(FULL, Le, src, LPS);
     k.H = __shfl_sync(FULL, He, src, LPS);
+    if (fixed) k.feas = (uint64_t)wmax + k.L <= (uint64_t)C.tau;
     k.thr = k.L < C.x_c ? C.x_c - k.L : 0u;
     if (k.L >= C.x_c) k.H = 0ull;
     return k;
@@ -281,7 +296,9 @@ __device__ __forceinline__ Cand cand_params(const Seg<LPS, MM> &sg, const SmemPr
   }
   k.feas = bits != 0u;
   k.e = k.feas ? 31u - __clz(bits) : (uint32_t)(__ffs(mbits) - 1);
+  if (fixed) k.e = fixed == 1 ? 31u - __clz(mbits) : (uint32_t)(__ffs(mbits) - 1);
   k.L = row[k.e * P.nb];
+  if (fixed) k.feas = (uint64_t)wmax + k.L <= (uint64_t)C.tau;
   k.thr = k.L < C.x_c ? C.x_c - k.L : 0u;
   k.H = k.L < C.x_c ? reinterpret_cast<const uint64_t *>(P.sm + C.off_H)[((size_t)gg * P.E + k.e) * P.nb + bi]
                     : 0ull;
@@ -335,6 +352,34 @@ __device__ __forceinline__ Decision finish_decision(const Seg<LPS, MM> &sg, cons
   d.S_own = S_own;
   d.m = mkey;
   const int src = (int)(mkey & (MM - 1)) * GL;
+  const uint32_t pk = sg.bcast(cand.e | (cand.feas ? 0x80u : 0u) | (cand.B << 8), src);
+  d.L = sg.bcast(cand.L, src);
+  d.e = pk & 0x7Fu;
+  d.feas = (pk & 0x80u) != 0u;
+  d.B = pk >> 8;
+  return d;
+}
+
+// LQF / EDF selection (ALL_FINAL, ALL_EARLY, EE_LQF: most queued tasks;
+// EE_EDF: least slack tau - w_head, i.e. the largest head wait; ties lowest m)
+// across the segment's groups; the winner's (e, B, L, feasible) from
+// cand_params; S = 0 (nothing is scored).  Whole warp.
+template <int LPS, int MM>
+__device__ __forceinline__ Decision select_simple(const Seg<LPS, MM> &sg, const Cand &cand, uint32_t len,
+                                                  uint32_t wmax, uint32_t policy) {
+  constexpr int GL = Seg<LPS, MM>::GL;
+  const uint64_t prim = policy == ES_POLICY_EE_EDF ? (uint64_t)wmax : (uint64_t)len;
+  uint64_t key = len ? (((prim + 1u) << 3) | (uint64_t)(7 - sg.grp)) : 0ull;  // empty queue: 0
+#pragma unroll
+  for (int o = GL; o < LPS; o <<= 1) {
+    const uint64_t ko = __shfl_xor_sync(FULL, key, o, LPS);
+    key = ko > key ? ko : key;
+  }
+  Decision d;
+  d.S = 0ull;
+  d.S_own = 0ull;
+  d.m = key ? 7u - (uint32_t)(key & 7u) : 0xFFu;
+  const int src = (int)(d.m & (MM - 1)) * GL;
   const uint32_t pk = sg.bcast(cand.e | (cand.feas ? 0x80u : 0u) | (cand.B << 8), src);
   d.L = sg.bcast(cand.L, src);
   d.e = pk & 0x7Fu;

@@ -29,8 +29,10 @@ struct __align__(16) CfgRec {
   uint32_t off_A, off_Bt, off_H, off_bidx;
   uint32_t status;    // ES_OK or ES_ERR_NUMERIC (set by k_build_tables)
   uint32_t fast_lim;  // x_c - max L over the profile (0 if <= 0): waits below it never clip
+  uint32_t policy;    // ES_POLICY_* (selection rule, Q26)
+  uint32_t pad[3];
 };
-static_assert(sizeof(CfgRec) == 64, "CfgRec layout");
+static_assert(sizeof(CfgRec) == 80, "CfgRec layout");
 
 struct ImgLayout {
   uint32_t bytes;  // total, multiple of 16
@@ -40,6 +42,7 @@ struct ImgLayout {
   // single-SLO specialisation of the K1 stream: byte offsets of A and Bt, 4 r,
   // and the A index mask 4 (2^k - 1) with 2^k >= nA_cap
   uint32_t c0_offA, c0_offBt, c0_r4, c0_amask;
+  uint32_t pol_mask;  // bit p set iff some cfg uses policy p (ES_POLICY_*)
 };
 
 // device-side sticky error record (per profile handle)

@@ -51,6 +51,8 @@ struct ReplayArgs {
   uint8_t *dec_f;
   DevStatus *dstat;
   unsigned long long *work;
+  bool any_simple;  // some cfg selects by LQF / EDF (baseline policies, Q26)
+  bool any_score;   // some cfg selects by the stability score (Eq. 7)
 };
 
 __device__ __forceinline__ uint32_t ldg_u32(const uint32_t *p) { return __ldg(p); }
@@ -222,8 +224,16 @@ __global__ void __launch_bounds__(256) k2_replay(const uint8_t *__restrict__ gim
       const Cand cand = cand_params<LPS, MM>(sg, P, C, len, wmax);
       const uint32_t tt = t;
       const uint32_t *Ah = Aq + head;
-      const Decision d =
-          decide<LPS, MM>(sg, P, C, len, c, b_slow == 0u, cand, [&](uint32_t p) { return tt - ldg_u32(Ah + p); });
+      // a5-a7: Eq. 7 on the stability score, or the LQF / EDF rule of a
+      // baseline policy (each runs warp-wide when some segment needs it)
+      const bool sc = policy_scores(C.policy);
+      Decision d{};
+      if (a.any_score && (!a.any_simple || __any_sync(FULL, dec && sc)))
+        d = decide<LPS, MM>(sg, P, C, len, c, b_slow == 0u, cand, [&](uint32_t p) { return tt - ldg_u32(Ah + p); });
+      if (a.any_simple && __any_sync(FULL, dec && !sc)) {
+        const Decision ds = select_simple<LPS, MM>(sg, cand, len, wmax, C.policy);
+        if (!sc) d = ds;
+      }
       const uint32_t ncand = __popc(sg.sbits(__ballot_sync(FULL, sg.gl == 0 && len > 0u)));
       // a8: commit
       const int src = (int)(d.m & (MM - 1)) * GL;
@@ -241,7 +251,7 @@ __global__ void __launch_bounds__(256) k2_replay(const uint8_t *__restrict__ gim
           if (sg.gl == 0 && len > 0u) {
             cells += nallow;
             live_sum += len - c;
-            terms += (uint64_t)(len - c) * ncand;
+            if (sc) terms += (uint64_t)(len - c) * ncand;  // Eq. 4 terms: scoring policies only
           }
           for (uint32_t j = sg.sl; j < d.B; j += LPS) {
             const uint64_t i = qb_w + head_w + j;
@@ -360,6 +370,10 @@ cudaError_t launch_replay(const uint8_t *img, const ImgLayout &lay, const es_tra
   a.dec_f = out.dec_flags;
   a.dstat = dstat;
   a.work = reinterpret_cast<unsigned long long *>(work_ctr);
+  constexpr uint32_t SCORE_POLS =
+      (1u << ES_POLICY_EDGESERVING) | (1u << ES_POLICY_ALLFINAL_DA) | (1u << ES_POLICY_OURS_BS1);
+  a.any_score = (lay.pol_mask & SCORE_POLS) != 0u;
+  a.any_simple = (lay.pol_mask & ~SCORE_POLS) != 0u;
   cudaError_t e = cudaMemsetAsync(work_ctr, 0, sizeof(unsigned long long), st);
   if (e != cudaSuccess) return e;
   *n_launch += 1;

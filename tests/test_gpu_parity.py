@@ -454,3 +454,55 @@ def test_k1_full_size_bench_batch():
     ok = g["flags"] & 6 == 0
     assert np.array_equal(np.argmin(cand[ok], axis=1), g["m"][ok].astype(np.int64))
     assert np.array_equal(cand[ok].min(axis=1), g["S"][ok])
+
+
+# ------------------------------------------------------------------ baseline / ablation policies (Q26)
+
+POLICY_IDS = {"edgeserving": 0, "all_final": 1, "all_early": 2, "ee_lqf": 3, "ee_edf": 4, "allfinal_da": 5,
+              "ours_bs1": 6}
+
+
+def with_policies(w, pols):
+    """The workload with one cfg per policy (same SLO knobs as cfg 0) and
+    scenario s on policy pols[s % len(pols)] -- segments of one warp mix
+    policies."""
+    import dataclasses
+    c0 = w.cfgs[0]
+    cfgs = [inputs.SchedCfg(tau=c0.tau, b_max=c0.b_max, C=c0.C, warmup=c0.warmup, policy=POLICY_IDS[p])
+            for p in pols]
+    ci = (np.arange(w.traces.n_scen) % len(pols)).astype(np.uint16)
+    return dataclasses.replace(w, cfgs=cfgs, traces=dataclasses.replace(w.traces, cfg_idx=ci))
+
+
+@pytest.mark.parametrize("policy", list(POLICY_IDS))
+def test_k2_policy_parity(policy):
+    """Every policy alone (cfg2 shape, 4 models x 4 exits, LPS 16; cfg3 shape,
+    8 models x 5 exits, LPS 32, bursty MMPP): completions, exits, latencies,
+    decision logs, counters and P95 bit-exact against the oracle."""
+    cap = 3000
+    for name, ids, n_req in [("cfg2", list(range(0, 60, 3)), 2000), ("cfg3", list(range(0, 45, 5)), 1500)]:
+        w = with_policies(inputs.workload(name, scen_ids=ids, n_req=n_req), [policy])
+        g = run_k2(w, dec_cap=cap)
+        o = oracle.replay_batch(w.profile, w.cfgs, w.traces, dec_cap=cap, nthreads=8)
+        assert g["_code"] == 0
+        assert_k2_equal(g, o, cap)
+
+
+def test_k2_mixed_policies_in_one_warp():
+    """All seven policies interleaved scenario by scenario (every warp mixes
+    scoring and LQF / EDF segments)."""
+    cap = 3000
+    w = with_policies(inputs.workload("cfg2", scen_ids=list(range(70)), n_req=1500), list(POLICY_IDS))
+    g = run_k2(w, dec_cap=cap)
+    o = oracle.replay_batch(w.profile, w.cfgs, w.traces, dec_cap=cap, nthreads=8)
+    assert g["_code"] == 0
+    assert_k2_equal(g, o, cap)
+
+
+def test_k1_rejects_baseline_policies():
+    """es_score_candidates scores EdgeServing only (include/edgeserve.h)."""
+    prof = inputs.synth_profile(2, 2, [1, 2])
+    h = es.es_load_profile(prof, [inputs.SchedCfg(tau=50000, b_max=2, policy=3)])
+    q_off, w = inputs.snapshots_uniform(1, 4, 2, 3, 100000)
+    with pytest.raises(es.EsError):
+        es.es_score_candidates(h, to_dev(q_off, torch.uint64), to_dev(w, torch.uint32))
