@@ -103,6 +103,10 @@ typedef struct {
  *   EE_EDF       least slack tau - w_head (largest head wait; ties lowest m), Eq. 5 / Eq. 6
  *   ALLFINAL_DA  Eq. 7 stability-score selection with every candidate at its deepest exit
  *   OURS_BS1     Algorithm 1 with B* = 1
+ *   SYMPHONY     deferred batching (Q27): deepest exit, B* of Eq. 5; a queue is
+ *                triggered when w_head + L >= tau or |Q| >= B_max; the triggered queue with the
+ *                largest w_head + L is served (ties lowest m); with none triggered the GPU idles
+ *                until the earliest trigger instant or the next arrival (not work-conserving)
  * A fixed exit is feasible iff w_head + L <= tau.  LQF / EDF policies score
  * nothing: the decision's S is 0.  Replay (es_replay_traces) accepts every
  * policy; es_score_candidates (K1) scores EdgeServing only (ES_ERR_ARG).
@@ -114,7 +118,8 @@ typedef struct {
 #define ES_POLICY_EE_EDF 4u
 #define ES_POLICY_ALLFINAL_DA 5u
 #define ES_POLICY_OURS_BS1 6u
-#define ES_POLICY_COUNT 7u
+#define ES_POLICY_SYMPHONY 7u
+#define ES_POLICY_COUNT 8u
 
 /*
  * Validate the profile (complete grid; L > 0; non-decreasing in batch;

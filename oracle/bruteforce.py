@@ -141,7 +141,7 @@ def tree_min_violations(arrivals, prof, tau, b_max):
 # the paper's baselines (§VI-A) and ablations (§VI-H),
 # read as DESIGN.md Q26; names as in SPEC's policy_decide
 POLICY_IDS = {"edgeserving": 0, "all_final": 1, "all_early": 2, "ee_lqf": 3, "ee_edf": 4, "allfinal_da": 5,
-              "ours_bs1": 6}
+              "ours_bs1": 6, "symphony": 7}
 
 
 def literal_policy_decide(prof, tau, C, b_max, waits, policy):
@@ -184,3 +184,53 @@ def literal_policy_decide(prof, tau, C, b_max, waits, policy):
     m_star = min(scores, key=lambda m: (scores[m], m))
     e, B, feas, _ = params(m_star)
     return m_star, e, B, feas, scores
+
+
+def symphony_replay_us(prof, tau, b_max, arrivals):
+    """Deferred batching (Symphony; Q27) simulated one
+    microsecond at a time -- no event jumps: whenever the GPU is free at
+    instant t, admit arrivals <= t; a queue is triggered when its head wait +
+    L(m, deepest allowed exit, B*) >= tau or it holds >= B_max tasks; the
+    triggered queue with the largest head wait + L is served (ties lowest m),
+    the batch runs exclusively for L; with none triggered the GPU stays idle
+    for one microsecond.  arrivals[m] = sorted list.  Returns the dispatch
+    list [(t, m, e, B)] and the completion time of every request."""
+    bs = [int(b) for b in prof.bs]
+    M = len(arrivals)
+    head = [0] * M
+    tail = [0] * M
+    done = [[None] * len(a) for a in arrivals]
+    total = sum(len(a) for a in arrivals)
+    served = 0
+    t = min(a[0] for a in arrivals if a)
+    out = []
+    while served < total:
+        for m in range(M):
+            while tail[m] < len(arrivals[m]) and arrivals[m][tail[m]] <= t:
+                tail[m] += 1
+        best, best_need = None, -1
+        for m in range(M):
+            n = tail[m] - head[m]
+            if n == 0:
+                continue
+            B = batch_size(n, b_max, bs)
+            e = max(i for i in range(prof.E) if prof.mask[m][i])
+            L = int(prof.lat[m, e, bs.index(B)])
+            need = t - arrivals[m][head[m]] + L
+            if (need >= tau or n >= b_max) and need > best_need:
+                best, best_need = m, need
+        if best is None:
+            t += 1
+            continue
+        m = best
+        n = tail[m] - head[m]
+        B = batch_size(n, b_max, bs)
+        e = max(i for i in range(prof.E) if prof.mask[m][i])
+        L = int(prof.lat[m, e, bs.index(B)])
+        out.append((t, m, e, B))
+        for i in range(head[m], head[m] + B):
+            done[m][i] = t + L
+        head[m] += B
+        served += B
+        t += L
+    return out, done

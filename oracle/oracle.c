@@ -54,11 +54,17 @@ enum { OR_OK = 0, OR_ERR_ARG = 1, OR_ERR_PROFILE = 2, OR_ERR_RANGE = 3, OR_ERR_U
  *   EE_EDF       least remaining slack tau - w_head (= largest head wait), Eq. 5 / 6
  *   ALLFINAL_DA  Eq. 7 stability-score selection, every candidate at its deepest exit
  *   OURS_BS1     Algorithm 1 with the batch fixed to 1 (bs[0])
- * LQF / EDF ties go to the lowest model index; those four policies score
- * nothing (S = 0).  A fixed exit is feasible iff w_head + L <= tau.
+ *   SYMPHONY     deferred batching (§VI-A; reading Q27): at the deepest
+ *                exit with B of Eq. 5, queue m is triggered when w_head + L >= tau
+ *                (one more idle microsecond would miss the SLO) or |Q_m| >= B_max;
+ *                the triggered queue with the largest w_head + L is dispatched
+ *                (ties lowest m); with none triggered the GPU idles until the
+ *                earliest trigger instant or the next arrival, whichever first
+ * LQF / EDF ties go to the lowest model index; those policies score nothing
+ * (S = 0).  A fixed exit is feasible iff w_head + L <= tau.
  */
 enum { OR_POL_EDGESERVING = 0, OR_POL_ALL_FINAL = 1, OR_POL_ALL_EARLY = 2, OR_POL_EE_LQF = 3,
-       OR_POL_EE_EDF = 4, OR_POL_ALLFINAL_DA = 5, OR_POL_OURS_BS1 = 6, OR_POL_N = 7 };
+       OR_POL_EE_EDF = 4, OR_POL_ALLFINAL_DA = 5, OR_POL_OURS_BS1 = 6, OR_POL_SYMPHONY = 7, OR_POL_N = 8 };
 
 /* ------------------------------------------------------------------ tables */
 
@@ -274,7 +280,8 @@ static int uses_score(const or_ctx *c) {
 static void cand_params(const or_ctx *c, int m, uint64_t len, uint64_t w_max, or_cand *out) {
   int bi = c->policy == OR_POL_OURS_BS1 ? 0 : batch_index(c, len);
   int e, feasible;
-  if (c->policy == OR_POL_ALL_FINAL || c->policy == OR_POL_ALLFINAL_DA || c->policy == OR_POL_ALL_EARLY) {
+  if (c->policy == OR_POL_ALL_FINAL || c->policy == OR_POL_ALLFINAL_DA || c->policy == OR_POL_ALL_EARLY ||
+      c->policy == OR_POL_SYMPHONY) {
     e = c->policy == OR_POL_ALL_EARLY ? shallowest_allowed(c, m) : deepest_allowed(c, m);
     feasible = w_max + LAT(c, m, e, bi) <= c->tau;
   } else {
@@ -376,6 +383,7 @@ int or_decide_batch(int M, int E, int nb, const int32_t *bs, const uint32_t *lat
     }
     if (k >= ncfg) { o_flags[s] = 4; continue; }
     const or_ctx *c = &ctx[k];
+    if (c->policy == OR_POL_SYMPHONY) { o_flags[s] = 4; continue; } /* replay-only policy (timer instants) */
     int bad = 0;
     for (int m = 0; m < M; ++m) {
       uint64_t lo = q_off[s * M + m], hi = q_off[s * M + m + 1];
@@ -480,7 +488,32 @@ static int replay_one(const or_ctx *c, const uint64_t *n, const uint32_t *const 
       for (uint64_t i = 0; i < len[m]; ++i) wbuf[m][i] = (uint32_t)(t - a[m][head[m] + i]);
     }
     int nc;
-    int best = decide(c, len, (const uint32_t *const *)wbuf, cands, &nc);
+    int best;
+    if (c->policy == OR_POL_SYMPHONY) {
+      /* deferred batching (Q27): dispatch only a triggered queue, else idle */
+      uint64_t wake = UINT64_MAX, best_need = 0;
+      best = -1;
+      nc = 0;
+      for (int m = 0; m < M; ++m) {
+        if (len[m] == 0) continue;
+        nc++;
+        cand_params(c, m, len[m], wbuf[m][0], &cands[m]);
+        uint64_t need = (uint64_t)wbuf[m][0] + cands[m].L; /* head latency if started now */
+        if (need >= c->tau || len[m] >= c->b_max) {
+          if (best < 0 || need > best_need) { best = m; best_need = need; }
+        } else if (t + (c->tau - need) < wake) {
+          wake = t + (c->tau - need); /* latest start that still meets tau */
+        }
+      }
+      if (best < 0) {
+        for (int m = 0; m < M; ++m)
+          if (tail[m] < n[m] && a[m][tail[m]] < wake) wake = a[m][tail[m]];
+        t = wake; /* idle until the earliest trigger or the next arrival */
+        continue;
+      }
+    } else {
+      best = decide(c, len, (const uint32_t *const *)wbuf, cands, &nc);
+    }
     const or_cand *d = &cands[best];
     if (t + d->L > 0xFFFFFFFFull) { status = OR_ERR_RANGE; break; }
     uint32_t done = (uint32_t)(t + d->L);

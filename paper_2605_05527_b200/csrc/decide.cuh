@@ -252,17 +252,20 @@ struct Cand {
 };
 
 // a3 + a4 for the group's own model g (valid when len > 0).  Whole warp.
-template <int LPS, int MM>
+// POL = false compiles Algorithm 1 only (C.policy ignored, no override code).
+template <int LPS, int MM, bool POL = false>
 __device__ __forceinline__ Cand cand_params(const Seg<LPS, MM> &sg, const SmemProf &P, const SmemCfg &C,
                                             uint32_t len, uint32_t wmax) {
   constexpr int GL = Seg<LPS, MM>::GL;
   Cand k;
   // Eq. 5 (OURS_BS1: B* = bs[0] = 1); fixed exits for ALL_FINAL / ALLFINAL_DA
   // (deepest allowed) and ALL_EARLY (shallowest allowed), else Eq. 6
-  const uint32_t cap = C.policy == ES_POLICY_OURS_BS1 ? 1u : (len < C.b_max ? len : C.b_max);
-  const int fixed = (C.policy == ES_POLICY_ALL_FINAL || C.policy == ES_POLICY_ALLFINAL_DA) ? 1
-                    : C.policy == ES_POLICY_ALL_EARLY                                    ? 2
-                                                                                         : 0;
+  const uint32_t cap = POL && C.policy == ES_POLICY_OURS_BS1 ? 1u : (len < C.b_max ? len : C.b_max);
+  const int fixed = !POL                                                                     ? 0
+                    : (C.policy == ES_POLICY_ALL_FINAL || C.policy == ES_POLICY_ALLFINAL_DA ||
+                       C.policy == ES_POLICY_SYMPHONY)                                       ? 1
+                    : C.policy == ES_POLICY_ALL_EARLY                                        ? 2
+                                                                                             : 0;
   const int gg = sg.grp < P.M ? sg.grp : 0;
   const uint32_t bi = P.sm[C.off_bidx + cap];
   k.B = P.bs[bi];
@@ -364,12 +367,18 @@ __device__ __forceinline__ Decision finish_decision(const Seg<LPS, MM> &sg, cons
 // EE_EDF: least slack tau - w_head, i.e. the largest head wait; ties lowest m)
 // across the segment's groups; the winner's (e, B, L, feasible) from
 // cand_params; S = 0 (nothing is scored).  Whole warp.
+// SYMPHONY (Q27): only triggered queues (w_head + L >= tau or |Q| >= B_max)
+// compete, by the largest w_head + L; none triggered -> d.m = 0xFF.
 template <int LPS, int MM>
 __device__ __forceinline__ Decision select_simple(const Seg<LPS, MM> &sg, const Cand &cand, uint32_t len,
-                                                  uint32_t wmax, uint32_t policy) {
+                                                  uint32_t wmax, const SmemCfg &C) {
   constexpr int GL = Seg<LPS, MM>::GL;
-  const uint64_t prim = policy == ES_POLICY_EE_EDF ? (uint64_t)wmax : (uint64_t)len;
-  uint64_t key = len ? (((prim + 1u) << 3) | (uint64_t)(7 - sg.grp)) : 0ull;  // empty queue: 0
+  const uint32_t policy = C.policy;
+  const uint64_t need = (uint64_t)wmax + cand.L;
+  const bool trig = need >= C.tau || len >= C.b_max;
+  const uint64_t prim = policy == ES_POLICY_EE_EDF ? (uint64_t)wmax : policy == ES_POLICY_SYMPHONY ? need : len;
+  const bool cand_ok = len && (policy != ES_POLICY_SYMPHONY || trig);
+  uint64_t key = cand_ok ? (((prim + 1u) << 3) | (uint64_t)(7 - sg.grp)) : 0ull;  // no candidate: 0
 #pragma unroll
   for (int o = GL; o < LPS; o <<= 1) {
     const uint64_t ko = __shfl_xor_sync(FULL, key, o, LPS);

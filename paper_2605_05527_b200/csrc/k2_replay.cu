@@ -81,7 +81,7 @@ __device__ __forceinline__ void report(DevStatus *ds, uint32_t code, int64_t ite
 #endif
 constexpr int PF_LINES = ES_PF_LINES;
 
-template <int LPS, int MM>
+template <int LPS, int MM, bool POL>
 __global__ void __launch_bounds__(256) k2_replay(const uint8_t *__restrict__ gimg, ImgLayout lay, ReplayArgs a) {
   constexpr int GL = Seg<LPS, MM>::GL;
   extern __shared__ __align__(16) uint8_t smem[];
@@ -157,7 +157,8 @@ __global__ void __launch_bounds__(256) k2_replay(const uint8_t *__restrict__ gim
     // ---- decisions until some segment of the warp drains its scenario
     for (;;) {
       // progress guard: each iteration serves >= 1 request or jumps to an arrival
-      if (active && status == ES_OK && ++iters > 2u * total + 4u) status = ES_ERR_INTERNAL;
+      // (deferred batching adds at most one idle step per arrival or dispatch)
+      if (active && status == ES_OK && ++iters > 4u * total + 8u) status = ES_ERR_INTERNAL;
       const bool run = active && status == ES_OK && served < total;
       // a2: admission (every arrival with a <= t)
       const bool pre_ok = run && head < tail;
@@ -221,25 +222,41 @@ __global__ void __launch_bounds__(256) k2_replay(const uint8_t *__restrict__ gim
         }
       }
       const uint32_t c = len ? live - head : 0u;
-      const Cand cand = cand_params<LPS, MM>(sg, P, C, len, wmax);
+      const Cand cand = cand_params<LPS, MM, POL>(sg, P, C, len, wmax);
       const uint32_t tt = t;
       const uint32_t *Ah = Aq + head;
       // a5-a7: Eq. 7 on the stability score, or the LQF / EDF rule of a
       // baseline policy (each runs warp-wide when some segment needs it)
-      const bool sc = policy_scores(C.policy);
+      const bool sc = !POL || policy_scores(C.policy);
       Decision d{};
-      if (a.any_score && (!a.any_simple || __any_sync(FULL, dec && sc)))
+      if (!POL || (a.any_score && (!a.any_simple || __any_sync(FULL, dec && sc))))
         d = decide<LPS, MM>(sg, P, C, len, c, b_slow == 0u, cand, [&](uint32_t p) { return tt - ldg_u32(Ah + p); });
-      if (a.any_simple && __any_sync(FULL, dec && !sc)) {
-        const Decision ds = select_simple<LPS, MM>(sg, cand, len, wmax, C.policy);
+      if (POL && a.any_simple && __any_sync(FULL, dec && !sc)) {
+        const Decision ds = select_simple<LPS, MM>(sg, cand, len, wmax, C);
         if (!sc) d = ds;
+      }
+      // SYMPHONY with no triggered queue (Q27): no dispatch; the GPU idles
+      // until the earliest trigger instant or the next arrival
+      bool disp = dec;
+      if (POL && a.any_simple) {
+        const bool sym = C.policy == ES_POLICY_SYMPHONY;
+        const bool wait = dec && sym && d.m == 0xFFu;
+        if (__any_sync(FULL, wait)) {
+          const uint64_t need = (uint64_t)wmax + cand.L;
+          const uint32_t rel = sg.vmin(wait && len > 0u ? (uint32_t)(C.tau - need) : 0xFFFFFFFFu);
+          const uint32_t na = sg.vmin(wait ? next_arr : 0xFFFFFFFFu);
+          if (wait) {
+            t = (uint32_t)min((uint64_t)t + rel, (uint64_t)na);
+            disp = false;
+          }
+        }
       }
       const uint32_t ncand = __popc(sg.sbits(__ballot_sync(FULL, sg.gl == 0 && len > 0u)));
       // a8: commit
       const int src = (int)(d.m & (MM - 1)) * GL;
       const uint64_t qb_w = sg.bcast(qb, src);
       const uint32_t head_w = sg.bcast(head, src);
-      if (dec) {
+      if (disp) {
         const uint64_t done64 = (uint64_t)t + d.L;
         if (done64 > 0xFFFFFFFFull) {
           status = ES_ERR_RANGE;
@@ -313,7 +330,8 @@ __global__ void __launch_bounds__(256) k2_replay(const uint8_t *__restrict__ gim
 
 template <int LPS, int MM>
 cudaError_t launch_t(const uint8_t *img, const ImgLayout &lay, const ReplayArgs &a, cudaStream_t st, int sms) {
-  auto kern = k2_replay<LPS, MM>;
+  // Algorithm 1 alone compiles without the policy code (no cost on the bench path)
+  auto kern = lay.pol_mask == (1u << ES_POLICY_EDGESERVING) ? k2_replay<LPS, MM, false> : k2_replay<LPS, MM, true>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lay.bytes);
   if (e != cudaSuccess) return e;
   int occ = 0;

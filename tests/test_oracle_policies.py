@@ -74,7 +74,7 @@ def _states(n, M, max_len, tau, seed):
     return q_off, w, st
 
 
-@pytest.mark.parametrize("policy", list(POL))
+@pytest.mark.parametrize("policy", [p for p in POL if p != "symphony"])
 def test_policies_vs_literal_bruteforce(policy):
     """600 seeded random states per policy (queues <= 10, waits in [0, 3 tau],
     sparse batch grid, one model with a restricted exit mask): model, exit,
@@ -148,3 +148,66 @@ def test_policy_replay_invariants(policy):
         assert np.all(o["dec_B"][:d] == 1) and d == n
     if POL[policy] in (1, 2, 3, 4):
         assert np.all(o["dec_S"][:d] == 0) and int(st[10]) == 0  # no Eq. 4 terms
+
+
+def _toy_traces(seed, M, n, span):
+    rng = np.random.default_rng(seed)
+    arr = [sorted(int(x) for x in rng.integers(0, span, rng.integers(1, n + 1))) for _ in range(M)]
+    off = np.zeros(M + 1, np.uint64)
+    off[1:] = np.cumsum([len(a) for a in arr])
+    tr = inputs.Traces(M=M, arr_off=off, arrival=np.concatenate([np.asarray(a, np.uint32) for a in arr]),
+                       cfg_idx=np.zeros(1, np.uint16), group_id=np.zeros(1, np.uint32))
+    return arr, tr
+
+
+def test_symphony_spec_example():
+    """single queue, oldest wait 10 ms, L(final, B) = 28 ms, tau = 50 ms
+    -> the dispatch waits 12 ms more: the request starts at a + 22 ms and
+    completes at a + 50 ms (T = tau, not a violation, Q16)."""
+    lat = np.array([[[9000, 12000], [28000, 40000]]], np.uint32)  # 1 model, exits {layer1, final}, batch {1, 2}
+    prof = inputs.Profile(M=1, E=2, bs=np.array([1, 2], np.int32), lat=lat, mask=np.ones((1, 2), np.uint8))
+    arr, tr = [[1000]], inputs.Traces(M=1, arr_off=np.array([0, 1], np.uint64), arrival=np.array([1000], np.uint32),
+                                      cfg_idx=np.zeros(1, np.uint16), group_id=np.zeros(1, np.uint32))
+    cfg = [inputs.SchedCfg(tau=50000, b_max=2, warmup=0, policy=POL["symphony"])]  # one task < B_max: defer
+    o = oracle.replay_batch(prof, cfg, tr, dec_cap=4)
+    assert int(o["dec_t"][0]) == 1000 + 22000 and int(o["dec_e"][0]) == 1
+    assert int(o["completion"][0]) == 1000 + 50000 and int(o["stats"][0][4]) == 0
+
+
+@pytest.mark.parametrize("seed", range(12))
+def test_symphony_vs_microsecond_simulation(seed):
+    """The oracle's event-jump Symphony replay (wake at the earliest trigger or
+    arrival) equals a microsecond-by-microsecond simulation of the same rule
+    (bruteforce.symphony_replay_us) on toy traces: every dispatch (t, m, e,
+    B) and every completion time."""
+    M = 1 + seed % 3
+    prof = inputs.synth_profile(M, 3, [1, 2, 4], L_top=9000.0)
+    arr, tr = _toy_traces(seed, M, 7, 60000)
+    tau, b_max = 20000 + 2000 * seed, 4
+    cfg = [inputs.SchedCfg(tau=tau, b_max=b_max, warmup=0, policy=POL["symphony"])]
+    o = oracle.replay_batch(prof, cfg, tr, dec_cap=64)
+    ref, done = bf.symphony_replay_us(prof, tau, b_max, arr)
+    d = int(o["stats"][0][0])
+    assert d == len(ref)
+    got = [(int(o["dec_t"][k]), int(o["dec_m"][k]), int(o["dec_e"][k]), int(o["dec_B"][k])) for k in range(d)]
+    assert got == ref
+    assert o["completion"].tolist() == [x for q in done for x in q]
+
+
+def test_symphony_never_dispatches_early():
+    """a dispatched batch's head would miss tau after one more idle
+    microsecond (w_head + L >= tau), unless its queue had reached B_max."""
+    w = inputs.workload("cfg2", scen_ids=[0, 5, 12], n_req=1500)
+    cfgs = [inputs.SchedCfg(tau=c.tau, b_max=c.b_max, policy=POL["symphony"]) for c in w.cfgs]
+    o = oracle.replay_batch(w.profile, cfgs, w.traces, dec_cap=2000)
+    M = w.profile.M
+    for s in range(3):
+        arr = [w.traces.arrival[int(w.traces.arr_off[s * M + m]):int(w.traces.arr_off[s * M + m + 1])]
+               for m in range(M)]
+        head = [0] * M
+        for k in range(int(o["stats"][s][0])):
+            t, m, B, L = (int(o[x][s * 2000 + k]) for x in ("dec_t", "dec_m", "dec_B", "dec_L"))
+            q = int(np.searchsorted(arr[m], t, side="right")) - head[m]
+            assert t - int(arr[m][head[m]]) + L >= cfgs[0].tau or q >= cfgs[0].b_max
+            assert int(o["dec_e"][s * 2000 + k]) == w.profile.E - 1
+            head[m] += B
