@@ -398,7 +398,7 @@ __device__ __forceinline__ Decision select_simple(const Seg<LPS, MM> &sg, const 
 }
 
 #ifndef ES_WU
-#define ES_WU 4
+#define ES_WU 2
 #endif
 constexpr int WU = ES_WU;  // positions per lane per step in the G loops
 

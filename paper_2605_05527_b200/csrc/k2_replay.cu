@@ -334,16 +334,23 @@ cudaError_t launch_t(const uint8_t *img, const ImgLayout &lay, const ReplayArgs 
   auto kern = lay.pol_mask == (1u << ES_POLICY_EDGESERVING) ? k2_replay<LPS, MM, false> : k2_replay<LPS, MM, true>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lay.bytes);
   if (e != cudaSuccess) return e;
+  // threads per block (ES_K2_BLOCK = 64 / 128 / 256): smaller blocks spread the
+  // scenarios' warps more evenly over the SMs when there is < 1 wave of them
+  int threads = 256;
+  if (const char *env = getenv("ES_K2_BLOCK")) {
+    const int v = atoi(env);
+    if (v == 64 || v == 128 || v == 256) threads = v;
+  }
   int occ = 0;
-  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 256, lay.bytes);
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, threads, lay.bytes);
   if (e != cudaSuccess) return e;
   if (occ < 1) return cudaErrorInvalidConfiguration;
-  constexpr int SEG_PER_BLOCK = 256 / LPS;
-  int64_t blocks = (a.n_scen + SEG_PER_BLOCK - 1) / SEG_PER_BLOCK;
+  const int seg_per_block = threads / LPS;
+  int64_t blocks = (a.n_scen + seg_per_block - 1) / seg_per_block;
   const int64_t cap = (int64_t)sms * occ;
   if (blocks > cap) blocks = cap;
   if (blocks < 1) blocks = 1;
-  kern<<<(unsigned)blocks, 256, lay.bytes, st>>>(img, lay, a);
+  kern<<<(unsigned)blocks, threads, lay.bytes, st>>>(img, lay, a);
   return cudaGetLastError();
 }
 
