@@ -152,6 +152,12 @@ def ncu_traffic(kernel):
     return None
 
 
+def ncu_issue(kernel):
+    """Issue-slot evidence of the last committed ncu --set full capture
+    (smsp__issue_active, sm__inst_executed; profiles/ncu_traffic.json)."""
+    return (ncu_traffic("_issue") or {}).get(kernel)
+
+
 def alg_ops(stats_sum, requests, E):
     """Algorithmic integer operations of Algorithm 1 per the op model of
     DESIGN.md §6: 3 per Eq. 4 term (predicted-wait add, clip compare,
@@ -365,6 +371,8 @@ def main():
             "k2_ms": statistics.mean(k2_ms), "k2_share_of_step": statistics.mean(k2_ms) / (ms / args.steps),
             "peak_source": f"148 SM x 128 INT32 lanes x {sm_max:.0f} MHz ({src} sm_max)",
             "alg_ops_per_launch": ops,
+            "issue_view": {"ncu": ncu_issue("k2_replay"), "decisions_per_launch": decisions_rank,
+                           "note": "latency-bound chain per scenario; smsp__issue_active from profiles/"},
             "hbm_view": {"alg_bytes_per_launch": alg_bytes, "achieved_gbs": alg_bytes / k2_avg_s / 1e9,
                          "peak_gbs": hbm, "frac": alg_bytes / k2_avg_s / 1e9 / hbm}}
 

@@ -107,6 +107,9 @@ typedef struct {
  *                triggered when w_head + L >= tau or |Q| >= B_max; the triggered queue with the
  *                largest w_head + L is served (ties lowest m); with none triggered the GPU idles
  *                until the earliest trigger instant or the next arrival (not work-conserving)
+ *   GRID         every admissible (m, e, b) -- allowed exit, profiled b <= min(|Q_m|, B_max) --
+ *                scored like Eq. 4 with L(m, e, b) and b served tasks; argmin of (S, m, e, b
+ *                index) (the north star's "1,280 candidates per decision", f2; Q28)
  * A fixed exit is feasible iff w_head + L <= tau.  LQF / EDF policies score
  * nothing: the decision's S is 0.  Replay (es_replay_traces) accepts every
  * policy; es_score_candidates (K1) scores EdgeServing only (ES_ERR_ARG).
@@ -119,7 +122,8 @@ typedef struct {
 #define ES_POLICY_ALLFINAL_DA 5u
 #define ES_POLICY_OURS_BS1 6u
 #define ES_POLICY_SYMPHONY 7u
-#define ES_POLICY_COUNT 8u
+#define ES_POLICY_GRID 8u
+#define ES_POLICY_COUNT 9u
 
 /*
  * Validate the profile (complete grid; L > 0; non-decreasing in batch;

@@ -111,7 +111,7 @@ def validate_profile(prof):
 
 # selection policies (oracle.c OR_POL_*, Q26)
 POLICIES = {"edgeserving": 0, "all_final": 1, "all_early": 2, "ee_lqf": 3, "ee_edf": 4, "allfinal_da": 5,
-            "ours_bs1": 6, "symphony": 7}
+            "ours_bs1": 6, "symphony": 7, "grid": 8}
 
 
 def _cfg_arrays(cfgs):

@@ -141,7 +141,7 @@ def tree_min_violations(arrivals, prof, tau, b_max):
 # the paper's baselines (§VI-A) and ablations (§VI-H),
 # read as DESIGN.md Q26; names as in SPEC's policy_decide
 POLICY_IDS = {"edgeserving": 0, "all_final": 1, "all_early": 2, "ee_lqf": 3, "ee_edf": 4, "allfinal_da": 5,
-              "ours_bs1": 6, "symphony": 7}
+              "ours_bs1": 6, "symphony": 7, "grid": 8}
 
 
 def literal_policy_decide(prof, tau, C, b_max, waits, policy):
@@ -234,3 +234,28 @@ def symphony_replay_us(prof, tau, b_max, arrivals):
         served += B
         t += L
     return out, done
+
+
+def literal_grid_decide(prof, tau, C, b_max, waits):
+    """GRID (f2): every admissible (m, e, b) -- allowed exit, profiled b <=
+    min(|Q_m|, B_max) -- scored by the literal float64 Eq. 3-4 on the
+    prediction of serving b tasks of Q_m at exit e; argmin of (S, m, e, b).
+    Returns (m, e, b, feasible, {(m, e, b): S}) or None."""
+    bs = [int(b) for b in prof.bs]
+    scores = {}
+    for m, q in enumerate(waits):
+        if not q:
+            continue
+        for e in range(prof.E):
+            if not prof.mask[m][e]:
+                continue
+            for bi, b in enumerate(bs):
+                if b > min(len(q), b_max):
+                    break
+                L = int(prof.lat[m, e, bi])
+                scores[(m, e, b)] = stability_score(predict(waits, m, b, L), tau, C)
+    if not scores:
+        return None
+    m, e, b = min(scores, key=lambda k: (scores[k], k))
+    L = int(prof.lat[m, e, bs.index(b)])
+    return m, e, b, waits[m][0] + L <= tau, scores

@@ -60,11 +60,16 @@ enum { OR_OK = 0, OR_ERR_ARG = 1, OR_ERR_PROFILE = 2, OR_ERR_RANGE = 3, OR_ERR_U
  *                the triggered queue with the largest w_head + L is dispatched
  *                (ties lowest m); with none triggered the GPU idles until the
  *                earliest trigger instant or the next arrival, whichever first
+ *   GRID         (north star's 1,280 candidates per decision; f2) every admissible
+ *                (m, e, b): allowed e, profiled b <= min(|Q_m|, B_max), scored
+ *                like Eq. 4 with L(m, e, b) and b served tasks; argmin of the
+ *                key (S, m, e, b index); feasible iff w_head + L <= tau
  * LQF / EDF ties go to the lowest model index; those policies score nothing
  * (S = 0).  A fixed exit is feasible iff w_head + L <= tau.
  */
 enum { OR_POL_EDGESERVING = 0, OR_POL_ALL_FINAL = 1, OR_POL_ALL_EARLY = 2, OR_POL_EE_LQF = 3,
-       OR_POL_EE_EDF = 4, OR_POL_ALLFINAL_DA = 5, OR_POL_OURS_BS1 = 6, OR_POL_SYMPHONY = 7, OR_POL_N = 8 };
+       OR_POL_EE_EDF = 4, OR_POL_ALLFINAL_DA = 5, OR_POL_OURS_BS1 = 6, OR_POL_SYMPHONY = 7, OR_POL_GRID = 8,
+       OR_POL_N = 9 };
 
 /* ------------------------------------------------------------------ tables */
 
@@ -272,7 +277,8 @@ static int shallowest_allowed(const or_ctx *c, int m) {
 }
 
 static int uses_score(const or_ctx *c) {
-  return c->policy == OR_POL_EDGESERVING || c->policy == OR_POL_ALLFINAL_DA || c->policy == OR_POL_OURS_BS1;
+  return c->policy == OR_POL_EDGESERVING || c->policy == OR_POL_ALLFINAL_DA || c->policy == OR_POL_OURS_BS1 ||
+         c->policy == OR_POL_GRID;
 }
 
 /* a3 + a4 of candidate m under the cfg's policy: batch (Eq. 5, or 1 for
@@ -291,11 +297,13 @@ static void cand_params(const or_ctx *c, int m, uint64_t len, uint64_t w_max, or
   out->S_q = 0; out->S_dbl = 0.0;
 }
 
-static void score_candidate(const or_ctx *c, int m, const uint64_t *len,
-                            const uint32_t *const *waits, or_cand *out) {
-  cand_params(c, m, len[m], waits[m][0], out);
-  int bi = out->bi, B = out->B, e = out->e;
-  uint32_t L = out->L;
+/* Eq. 4 on the predicted state of serving b = bs[bi] tasks of Q_m at exit e */
+static void score_at(const or_ctx *c, int m, int e, int bi, const uint64_t *len, const uint32_t *const *waits,
+                     or_cand *out) {
+  int B = c->bs[bi];
+  uint32_t L = LAT(c, m, e, bi);
+  out->e = e; out->bi = bi; out->B = B; out->L = L;
+  out->feasible = (uint64_t)waits[m][0] + L <= c->tau;
   uint64_t K = 0;
   unsigned __int128 U = 0;
   double S_dbl = 0.0;
@@ -318,6 +326,14 @@ static void score_candidate(const or_ctx *c, int m, const uint64_t *len,
   out->S_q = S; out->S_dbl = S_dbl;
 }
 
+static void score_candidate(const or_ctx *c, int m, const uint64_t *len,
+                            const uint32_t *const *waits, or_cand *out) {
+  cand_params(c, m, len[m], waits[m][0], out);
+  int feasible = out->feasible;
+  score_at(c, m, out->e, out->bi, len, waits, out);
+  out->feasible = feasible; /* Eq. 6's flag (Q2) */
+}
+
 /*
  * decide() on one snapshot (Algorithm 1; Eq. 7 argmin with
  * tie-break lowest model index, Q3; or the cfg's baseline policy, Q26).
@@ -328,6 +344,26 @@ static int decide(const or_ctx *c, const uint64_t *len, const uint32_t *const *w
                   or_cand *cands /* [M] */, int *n_cand) {
   int best = -1;
   *n_cand = 0;
+  if (c->policy == OR_POL_GRID) {
+    /* every admissible (m, e, b), in (m, e, b) order: strict < keeps the
+       lowest (m, e, b index) on equal scores */
+    or_cand x;
+    for (int m = 0; m < c->M; ++m) {
+      if (len[m] == 0) continue;
+      int have = 0; /* cands[m] = model m's best cell */
+      uint64_t cap = len[m] < c->b_max ? len[m] : c->b_max;
+      for (int e = 0; e < c->E; ++e) {
+        if (!allowed(c, m, e)) continue;
+        for (int bi = 0; bi < c->nb && (uint64_t)c->bs[bi] <= cap; ++bi) {
+          score_at(c, m, e, bi, len, waits, &x);
+          (*n_cand)++;
+          if (!have || x.S_q < cands[m].S_q) { cands[m] = x; have = 1; }
+        }
+      }
+      if (best < 0 || cands[m].S_q < cands[best].S_q) best = m;
+    }
+    return best;
+  }
   if (uses_score(c)) {
     for (int m = 0; m < c->M; ++m) {
       if (len[m] == 0) continue;

@@ -402,6 +402,78 @@ __device__ __forceinline__ Decision select_simple(const Seg<LPS, MM> &sg, const 
 #endif
 constexpr int WU = ES_WU;  // positions per lane per step in the G loops
 
+// f2 GRID (Q28): every admissible (m, e, b) of every segment, in a
+// warp-uniform (m, e, b index) sweep with per-segment validity; per cell the
+// segment's lanes count K / sum U over their group's live positions (own
+// queue: the b served positions excluded), the clipped-for-everyone
+// prefixes are counted from the indices; running argmin of (S, cell index).
+// ncells = admissible cells of this segment.  Whole warp.
+template <int LPS, int MM, class WaitAt>
+__device__ __noinline__ Decision decide_grid(const Seg<LPS, MM> &sg, const SmemProf &P, const SmemCfg &C,
+                                             uint32_t len, uint32_t c, uint32_t wmax, WaitAt wait_at,
+                                             uint32_t &ncells) {
+  constexpr int GL = Seg<LPS, MM>::GL;
+  uint64_t bS = ~0ull;
+  uint32_t bidx = 0xFFFFFFFFu, bm = 0xFFu, be = 0u, bB = 0u, bL = 0u;
+  bool bfeas = false;
+  ncells = 0u;
+  const uint32_t cpre = sg.sum(sg.gl == 0 ? c : 0u);
+  const uint64_t *Hq = reinterpret_cast<const uint64_t *>(P.sm + C.off_H);
+  for (int m = 0; m < P.M; ++m) {
+    const uint32_t len_m = sg.bcast(len, m * GL), c_m = sg.bcast(c, m * GL), wmax_m = sg.bcast(wmax, m * GL);
+    const uint32_t cap = len_m < C.b_max ? len_m : C.b_max;
+    for (int e = 0; e < P.E; ++e) {
+      const bool ok_e = len_m > 0u && ((P.mask[m] >> e) & 1u);
+      for (int bi = 0; bi < P.nb; ++bi) {
+        const uint32_t b = P.bs[bi];
+        const bool valid = ok_e && b <= cap;
+        if (!__any_sync(FULL, valid)) continue;  // (bs increasing: no later bi either for this segment)
+        const int cell = (m * P.E + e) * P.nb + bi;
+        const uint32_t L = P.lat[cell];
+        const uint32_t thr = L < C.x_c ? C.x_c - L : 0u;
+        uint32_t K = 0u;
+        uint64_t U = 0ull;
+        if (valid)
+          for (uint32_t p = c + sg.gl; p < len; p += GL) {
+            if (sg.grp == m && p < b) continue;  // candidate m's own served tasks
+            const uint32_t w = wait_at(p);
+            if (w >= thr) K += 1u;
+            else U += G_of(P, C, w);
+          }
+        K = sg.sum(K);
+        U = sg.sum64(U);
+        if (valid) {
+          const uint64_t Kt = (uint64_t)K + (uint64_t)(cpre - (c_m < b ? c_m : b));
+          uint64_t S = C.C_q * Kt;
+          if (L < C.x_c) {
+            const uint64_t H = Hq[cell], lo = H * U, hi = __umul64hi(H, U);
+            S += (hi << (64 - F)) | (lo >> F);
+          }
+          ncells++;
+          if (S < bS || (S == bS && (uint32_t)cell < bidx)) {
+            bS = S;
+            bidx = (uint32_t)cell;
+            bm = (uint32_t)m;
+            be = (uint32_t)e;
+            bB = b;
+            bL = L;
+            bfeas = (uint64_t)wmax_m + L <= (uint64_t)C.tau;
+          }
+        }
+      }
+    }
+  }
+  Decision dd;
+  dd.S = bS;
+  dd.S_own = bS;
+  dd.m = bm;
+  dd.e = be;
+  dd.B = bB;
+  dd.L = bL;
+  dd.feas = bfeas;
+  return dd;
+}
+
 template <int LPS, int MM, class WaitAt>
 __device__ __forceinline__ Decision decide_general(const Seg<LPS, MM> &sg, const SmemProf &P, const SmemCfg &C,
                                                 uint32_t len, uint32_t c, const Cand &cand, uint32_t Bown,

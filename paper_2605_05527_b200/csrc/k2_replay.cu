@@ -51,8 +51,9 @@ struct ReplayArgs {
   uint8_t *dec_f;
   DevStatus *dstat;
   unsigned long long *work;
-  bool any_simple;  // some cfg selects by LQF / EDF (baseline policies, Q26)
+  bool any_simple;  // some cfg selects by LQF / EDF / deferred batching (Q26, Q27)
   bool any_score;   // some cfg selects by the stability score (Eq. 7)
+  bool any_grid;    // some cfg scores every (m, e, b) cell (f2, Q28)
 };
 
 __device__ __forceinline__ uint32_t ldg_u32(const uint32_t *p) { return __ldg(p); }
@@ -235,6 +236,17 @@ __global__ void __launch_bounds__(256) k2_replay(const uint8_t *__restrict__ gim
         const Decision ds = select_simple<LPS, MM>(sg, cand, len, wmax, C);
         if (!sc) d = ds;
       }
+      const bool grid = POL && C.policy == ES_POLICY_GRID;
+      uint32_t ngrid = 0u;
+      if (POL && a.any_grid && __any_sync(FULL, dec && grid)) {
+        uint32_t ng = 0u;
+        const Decision dg = decide_grid<LPS, MM>(sg, P, C, len, c, wmax, [&](uint32_t p) { return tt - ldg_u32(Ah + p); },
+                                                 ng);
+        if (grid) {
+          d = dg;
+          ngrid = ng;
+        }
+      }
       // SYMPHONY with no triggered queue (Q27): no dispatch; the GPU idles
       // until the earliest trigger instant or the next arrival
       bool disp = dec;
@@ -251,7 +263,8 @@ __global__ void __launch_bounds__(256) k2_replay(const uint8_t *__restrict__ gim
           }
         }
       }
-      const uint32_t ncand = __popc(sg.sbits(__ballot_sync(FULL, sg.gl == 0 && len > 0u)));
+      const uint32_t nq = __popc(sg.sbits(__ballot_sync(FULL, sg.gl == 0 && len > 0u)));
+      const uint32_t ncand = grid ? ngrid : nq;  // scored candidates: queues, or (m, e, b) cells
       // a8: commit
       const int src = (int)(d.m & (MM - 1)) * GL;
       const uint64_t qb_w = sg.bcast(qb, src);
@@ -268,7 +281,7 @@ __global__ void __launch_bounds__(256) k2_replay(const uint8_t *__restrict__ gim
           if (sg.gl == 0 && len > 0u) {
             cells += nallow;
             live_sum += len - c;
-            if (sc) terms += (uint64_t)(len - c) * ncand;  // Eq. 4 terms: scoring policies only
+            if (sc || grid) terms += (uint64_t)(len - c) * ncand;  // Eq. 4 terms: scoring policies only
           }
           for (uint32_t j = sg.sl; j < d.B; j += LPS) {
             const uint64_t i = qb_w + head_w + j;
@@ -397,8 +410,10 @@ cudaError_t launch_replay(const uint8_t *img, const ImgLayout &lay, const es_tra
   a.work = reinterpret_cast<unsigned long long *>(work_ctr);
   constexpr uint32_t SCORE_POLS =
       (1u << ES_POLICY_EDGESERVING) | (1u << ES_POLICY_ALLFINAL_DA) | (1u << ES_POLICY_OURS_BS1);
+  constexpr uint32_t GRID_POLS = 1u << ES_POLICY_GRID;
   a.any_score = (lay.pol_mask & SCORE_POLS) != 0u;
-  a.any_simple = (lay.pol_mask & ~SCORE_POLS) != 0u;
+  a.any_grid = (lay.pol_mask & GRID_POLS) != 0u;
+  a.any_simple = (lay.pol_mask & ~(SCORE_POLS | GRID_POLS)) != 0u;
   cudaError_t e = cudaMemsetAsync(work_ctr, 0, sizeof(unsigned long long), st);
   if (e != cudaSuccess) return e;
   *n_launch += 1;

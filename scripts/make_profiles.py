@@ -46,6 +46,13 @@ for tag, kern in [("k2", "k2_replay"), ("k3", "k3_stats"), ("k1", "k1_call")]:
         u = uu[hh.index(m)]
         return x * {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(u, 1)
     total = 0.0
+    issue = {}
+    for row in rr[2:]:
+        nm = row[hh.index("Kernel Name")].split("(")[0].split("::")[-1].split("<")[0].replace("void ", "").strip()
+        issue[nm] = {"issue_active_pct": float(row[hh.index("smsp__issue_active.avg.pct_of_peak_sustained_active")]
+                                                .replace(",", "")),
+                     "warp_inst": val(row, "sm__inst_executed.sum") if "sm__inst_executed.sum" in hh else None}
+    traffic.setdefault("_issue", {}).update(issue)
     for row in rr[2:]:  # one row per captured launch (K1: the four kernels of one call)
         b = val(row, "dram__bytes_read.sum") + val(row, "dram__bytes_write.sum")
         name = row[hh.index("Kernel Name")].split("(")[0].split("::")[-1].split("<")[0].strip()

@@ -13,7 +13,7 @@ import inputs, paper_2605_05527_b200 as es
 from paper_2605_05527_b200 import engine
 
 POL = {"edgeserving": 0, "all_final": 1, "all_early": 2, "ee_lqf": 3, "ee_edf": 4, "allfinal_da": 5, "ours_bs1": 6,
-       "symphony": 7}
+       "symphony": 7, "grid": 8}
 w = inputs.workload("cfg2")
 dtr = engine.upload_traces(w.traces, "cuda")
 G = inputs.n_groups("cfg2")

@@ -459,7 +459,7 @@ def test_k1_full_size_bench_batch():
 # ------------------------------------------------------------------ baseline / ablation policies (Q26)
 
 POLICY_IDS = {"edgeserving": 0, "all_final": 1, "all_early": 2, "ee_lqf": 3, "ee_edf": 4, "allfinal_da": 5,
-              "ours_bs1": 6, "symphony": 7}
+              "ours_bs1": 6, "symphony": 7, "grid": 8}
 
 
 def with_policies(w, pols):
@@ -489,7 +489,7 @@ def test_k2_policy_parity(policy):
 
 
 def test_k2_mixed_policies_in_one_warp():
-    """All eight policies interleaved scenario by scenario (every warp mixes
+    """All nine policies interleaved scenario by scenario (every warp mixes
     scoring and LQF / EDF segments)."""
     cap = 3000
     w = with_policies(inputs.workload("cfg2", scen_ids=list(range(70)), n_req=1500), list(POLICY_IDS))
