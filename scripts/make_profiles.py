@@ -51,7 +51,7 @@ for tag, kern in [("k2", "k2_replay"), ("k3", "k3_stats"), ("k1", "k1_call")]:
         nm = row[hh.index("Kernel Name")].split("(")[0].split("::")[-1].split("<")[0].replace("void ", "").strip()
         issue[nm] = {"issue_active_pct": float(row[hh.index("smsp__issue_active.avg.pct_of_peak_sustained_active")]
                                                 .replace(",", "")),
-                     "warp_inst": val(row, "sm__inst_executed.sum") if "sm__inst_executed.sum" in hh else None}
+                     "warp_inst": val(row, "smsp__inst_executed.sum") if "smsp__inst_executed.sum" in hh else None}
     traffic.setdefault("_issue", {}).update(issue)
     for row in rr[2:]:  # one row per captured launch (K1: the four kernels of one call)
         b = val(row, "dram__bytes_read.sum") + val(row, "dram__bytes_write.sum")
