@@ -63,6 +63,12 @@ struct StreamArgs {
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 
+__device__ __forceinline__ uint64_t wsum64_pre(uint64_t v) {
+#pragma unroll
+  for (int o = 16; o >= 1; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
 __global__ void __launch_bounds__(256) k1s_prep(const uint8_t *__restrict__ gimg, ImgLayout lay, StreamArgs a) {
   pdl_trigger();
   extern __shared__ __align__(16) uint8_t smem[];
@@ -71,20 +77,25 @@ __global__ void __launch_bounds__(256) k1s_prep(const uint8_t *__restrict__ gimg
   const SmemProf P = smem_prof(smem, lay);
   const int M = P.M;
   const int64_t nq = a.n * M;
-  for (int64_t qi = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; qi < nq; qi += (int64_t)gridDim.x * blockDim.x) {
+  const int lane = threadIdx.x & 31;
+  // warp-uniform sweep: lane l of a warp prepares queue base + l
+  for (int64_t q0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) & ~31ll; q0 < nq;
+       q0 += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t qi = q0 + lane;
+    const bool on = qi < nq;
     const int64_t s = qi / M;
     const int g = (int)(qi - s * M);
-    const int k = a.cfg_idx ? (int)a.cfg_idx[s] : 0;
+    const int k = on ? (a.cfg_idx ? (int)a.cfg_idx[s] : 0) : 0;
     QRec r{};
-    if (k >= P.ncfg) {
-      atomicOr(a.acc + s * ACC + 1, F_BAD);
-      a.rec[qi] = r;
-      continue;
+    uint32_t nsv = 0u;
+    SmemCfg C{};
+    if (on && k >= P.ncfg) atomicOr(a.acc + s * ACC + 1, F_BAD);
+    if (on && k < P.ncfg) {
+      C = smem_cfg(P, k);
+      r.lo = a.q_off[qi];
+      r.len = (uint32_t)(a.q_off[qi + 1] - r.lo);
     }
-    const SmemCfg C = smem_cfg(P, k);
-    r.lo = a.q_off[qi];
-    r.len = (uint32_t)(a.q_off[qi + 1] - r.lo);
-    if (r.len) {
+    if (on && k < P.ncfg && r.len) {
       const uint32_t *W = a.waits + r.lo;
       const uint32_t wmax = __ldg(W);
       if (wmax >= C.x_c) {  // clipped-for-everyone prefix: first position with w < x_c
@@ -109,18 +120,39 @@ __global__ void __launch_bounds__(256) k1s_prep(const uint8_t *__restrict__ gimg
       r.ef = e | (best >= 0 ? 0x80u : 0u);
       r.thr = r.L < C.x_c ? C.x_c - r.L : 0u;
       r.H = r.L < C.x_c ? reinterpret_cast<const uint64_t *>(P.sm + C.off_H)[((size_t)g * P.E + e) * P.nb + bi] : 0ull;
-      // own served head for the fast path (the clip path excludes it per task)
-      const uint32_t nsv = r.B < r.len ? r.B : r.len;
-      uint64_t sv = G_of(P, C, wmax);
-#pragma unroll 8
-      for (uint32_t j = 1; j < nsv; ++j) sv += G_of(P, C, __ldg(W + j));
-      r.srv = sv;
+      nsv = r.B < r.len ? r.B : r.len;
       if (wmax >= C.fast_lim || C.x_c > V4_LIM) {
         const unsigned long long was = atomicOr(a.acc + s * ACC + 1, F_SLOW);
         if (!(was & F_SLOW)) a.slow_list[atomicAdd(a.slow_n, 1ull)] = s;
       }
     }
-    a.rec[qi] = r;
+    // own served heads for the fast path (the clip path excludes them
+    // per task): the warp reads its 32 queues' first min(B*, len) waits with
+    // coalesced loads, 8 queues' loads in flight at a time
+    uint64_t mine = 0;
+    if (__any_sync(FULL, nsv > 0u)) {
+#pragma unroll 1
+      for (int u0 = 0; u0 < 32; u0 += 8) {
+        uint32_t wv[8], nn[8];
+        uint64_t lo8[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          lo8[u] = __shfl_sync(FULL, r.lo, u0 + u);
+          nn[u] = __shfl_sync(FULL, nsv, u0 + u);
+          wv[u] = (uint32_t)lane < nn[u] ? __ldg(a.waits + lo8[u] + lane) : 0u;
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const SmemCfg Cs = smem_cfg(P, __shfl_sync(FULL, k, u0 + u) < P.ncfg ? __shfl_sync(FULL, k, u0 + u) : 0);
+          uint64_t sv = (uint32_t)lane < nn[u] ? (uint64_t)G_of(P, Cs, wv[u]) : 0ull;
+          for (uint32_t j = 32u + lane; j < nn[u]; j += 32u) sv += G_of(P, Cs, __ldg(a.waits + lo8[u] + j));  // B* > 32
+          sv = wsum64_pre(sv);
+          if (lane == u0 + u) mine = sv;
+        }
+      }
+    }
+    r.srv = mine;
+    if (on) a.rec[qi] = r;
   }
 }
 
