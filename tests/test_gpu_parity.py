@@ -506,3 +506,24 @@ def test_k1_rejects_baseline_policies():
     q_off, w = inputs.snapshots_uniform(1, 4, 2, 3, 100000)
     with pytest.raises(es.EsError):
         es.es_score_candidates(h, to_dev(q_off, torch.uint64), to_dev(w, torch.uint32))
+
+
+@pytest.mark.parametrize("fast", ["tma", "regs"])
+def test_k1_stream_large_image(monkeypatch, fast):
+    """Deep snapshots under cfg3's nine SLOs (20..100 ms): the profile image
+    is ~145 KB, so the TMA ring drops to 2 KB pieces x 2 slots (and the
+    register-pipelined kernel is the ES_K1_FAST=regs variant); per-snapshot
+    SLO index, mixed fast / clip-path snapshots (short SLOs clip)."""
+    monkeypatch.setenv("ES_K1", "stream")
+    monkeypatch.setenv("ES_K1_FAST", fast)
+    w = inputs.workload("cfg3", scen_ids=[0], n_req=10)
+    M = 8
+    n = 270
+    q_off, wts = inputs.snapshots_poisson_depth(21, np.arange(n), M, 1600, [1600 / 90000.0] * M)
+    ci = (np.arange(n) % 9).astype(np.uint16)
+    h = es.es_load_profile(w.profile, w.cfgs)
+    o = es.es_score_candidates(h, to_dev(q_off, torch.uint64), to_dev(wts, torch.uint32), to_dev(ci, torch.uint16))
+    torch.cuda.synchronize()
+    g = {k: np_of(v) for k, v in o.items()}
+    ref = oracle.decide_batch(w.profile, w.cfgs, q_off, wts, ci)
+    assert_k1_equal(g, ref, M)
