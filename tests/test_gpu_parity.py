@@ -527,3 +527,28 @@ def test_k1_stream_large_image(monkeypatch, fast):
     g = {k: np_of(v) for k, v in o.items()}
     ref = oracle.decide_batch(w.profile, w.cfgs, q_off, wts, ci)
     assert_k1_equal(g, ref, M)
+
+
+def test_k1_stream_extreme_shapes(monkeypatch):
+    """The TMA streaming mapping on its edge shapes: one snapshot with a single
+    3M-wait queue (every warp range inside one queue, no boundary) and 20,000
+    snapshots of 0-3 waits per queue (several queue and snapshot boundaries
+    in every 128-wait window, empty queues and empty snapshots)."""
+    monkeypatch.setenv("ES_K1", "stream")
+    M = 8
+    prof = inputs.synth_profile(M, 5, list(range(1, 33)))
+    cfgs = [inputs.SchedCfg(tau=50000, b_max=32)]
+    h = es.es_load_profile(prof, cfgs)
+    # one deep queue: waits non-increasing, all live (< fast_lim)
+    n_big = 3_000_000
+    w = (np.arange(n_big, 0, -1, dtype=np.int64) * 120000 // n_big).astype(np.uint32)
+    q_off = np.zeros(M + 1, np.uint64)
+    q_off[3:] = n_big
+    o = es.es_score_candidates(h, to_dev(q_off, torch.uint64), to_dev(w, torch.uint32))
+    torch.cuda.synchronize()
+    assert_k1_equal({k: np_of(v) for k, v in o.items()}, oracle.decide_batch(prof, cfgs, q_off, w), M)
+    # many tiny snapshots
+    q_off, w = inputs.snapshots_uniform(77, 20000, M, 3, 100000)
+    o = es.es_score_candidates(h, to_dev(q_off, torch.uint64), to_dev(w, torch.uint32))
+    torch.cuda.synchronize()
+    assert_k1_equal({k: np_of(v) for k, v in o.items()}, oracle.decide_batch(prof, cfgs, q_off, w), M)
