@@ -461,42 +461,61 @@ __global__ void __launch_bounds__(TMA_NW * 32, 1) k1s_stream_tma(const uint8_t *
     lo += step * l;
     hi = min(hi, lo + step);
   }
-  // queue record q of snapshot s spread over the lanes (see k1s_stream_fast)
-  auto fetch = [&](int64_t q, int64_t s) -> uint32_t {
-    if (q >= nq) return 0u;
-    if (lane < 10) return __ldg(reinterpret_cast<const uint32_t *>(a.rec + q) + lane);
-    if (lane == 10) return (uint32_t)a.acc[s * ACC + 1];  // F_SLOW is final (set by k1s_prep)
-    if (lane == 11) return a.cfg_idx ? (uint32_t)a.cfg_idx[s] : 0u;
-    return 0u;
-  };
-  pdl_wait();  // k1s_prep's records and flags
+  pdl_wait();  // k1s_prep's snapshot flags
   constexpr int32_t BIG = 0x3FFFFFFF;
   const int32_t rend_full = (int32_t)(4 * (min(v1, nfull) - v0));  // fast windows end here
   int64_t qi = lo, s_cur = lo / M;
   int m_cur = (int)(lo - s_cur * M);
-  uint32_t dnext = m_cur + 1 < M ? fetch(qi + 1, s_cur) : fetch(qi + 1, s_cur + 1);
+  // queue and snapshot descriptors in warp-distributed register windows, the
+  // next window loaded 32 entries ahead (no dependent load per queue):
+  //   qw_*: lane l holds q_off[qb + l] (q_off[nq] past the end)
+  //   fw_*: lane l holds F_SLOW | cfg << 1 of snapshot sb + l (final after k1s_prep)
+  auto qload = [&](int64_t b) -> uint64_t { return b + lane <= nq ? __ldg(a.q_off + b + lane) : end; };
+  auto fload = [&](int64_t b) -> uint32_t {
+    const int64_t sx = b + lane;
+    if (sx >= a.n) return 0u;
+    const uint32_t k = a.cfg_idx ? (uint32_t)a.cfg_idx[sx] : 0u;
+    return (uint32_t)(a.acc[sx * ACC + 1] & F_SLOW) | (k << 1);
+  };
+  int64_t qb = qi, sb = s_cur;
+  uint64_t qw_cur = qload(qb), qw_nxt = qload(qb + 32);
+  uint32_t fw_cur = fload(sb), fw_nxt = fload(sb + 32);
+  auto qoff = [&](int64_t q) -> uint64_t {  // q in [qb, qb + 32]
+    const int d = (int)(q - qb);
+    const uint64_t x = __shfl_sync(FULL, qw_cur, d & 31), y = __shfl_sync(FULL, qw_nxt, 0);
+    return d < 32 ? x : y;
+  };
   // warp-uniform queue state (range-relative positions)
   int32_t qs_r = 0, qe_r = 0, lo_r = BIG, hi_r = -BIG;
   bool skip = true;
   GTab Gg{0u, 0u, 0u, 0u};
   const GOne G1{sbase + lay.c0_offA, sbase + lay.c0_offBt, lay.c0_r4, lay.c0_amask};
   auto clampr = [&](int64_t p) -> int32_t { return (int32_t)max(min(p - R0, (int64_t)BIG), -(int64_t)BIG); };
-  auto set_queue = [&](uint32_t d, bool new_snap) {
-    const uint64_t rlo = (uint64_t)__shfl_sync(FULL, d, 0) | ((uint64_t)__shfl_sync(FULL, d, 1) << 32);
-    const uint32_t rlen = __shfl_sync(FULL, d, 4);
-    const uint32_t flg = __shfl_sync(FULL, d, 10), k = __shfl_sync(FULL, d, 11);
+  auto set_queue = [&](bool new_snap) {
+    if (qi - qb >= 32) {  // slide the queue window
+      qb += 32;
+      qw_cur = qw_nxt;
+      qw_nxt = qload(qb + 32);
+    }
+    if (s_cur - sb >= 32) {  // slide the snapshot window
+      sb += 32;
+      fw_cur = fw_nxt;
+      fw_nxt = fload(sb + 32);
+    }
+    const uint64_t rlo = qoff(qi), rhi = qoff(qi + 1);
+    const uint32_t fk = __shfl_sync(FULL, fw_cur, (int)(s_cur - sb));
+    const uint32_t k = fk >> 1;
     if (!ONE && new_snap && k < (uint32_t)P.ncfg) {
       const SmemCfg C = smem_cfg(P, (int)k);
       Gg = GTab{sbase + C.off_A, sbase + C.off_Bt, 4u * C.r, C.nA1};
     }
-    // rec is zero for an out-of-range cfg (k1s_prep): rlen = 0, the queue is skipped
-    skip = (flg & (uint32_t)F_SLOW) != 0u || rlen == 0u || k >= (uint32_t)P.ncfg;
+    skip = (fk & 1u) != 0u || rhi == rlo || k >= (uint32_t)P.ncfg;
     qs_r = clampr((int64_t)rlo);
-    qe_r = clampr((int64_t)(rlo + rlen));
-    lo_r = skip ? BIG : qs_r + 1;
+    qe_r = clampr((int64_t)rhi);
+    lo_r = skip ? BIG : qs_r;  // a window starting at the head: its first pair is cross-queue (qstart)
     hi_r = min(qe_r, rend_full) - 128;
   };
-  set_queue(fetch(qi, s_cur), true);
+  set_queue(true);
   uint64_t tot = 0;
   uint32_t bad = 0u;
   auto Gv = [&](uint32_t w) -> uint32_t { return ONE ? G1(w) : Gg(w); };
@@ -518,20 +537,18 @@ __global__ void __launch_bounds__(TMA_NW * 32, 1) k1s_stream_tma(const uint8_t *
       lo_r = BIG;
       return;
     }
-    const uint32_t d = dnext;
     const bool ns = ++m_cur == M;
     if (ns) {
       flush_snap();
       m_cur = 0;
       ++s_cur;
     }
-    dnext = m_cur + 1 < M ? fetch(qi + 1, s_cur) : fetch(qi + 1, s_cur + 1);
-    set_queue(d, ns);
+    set_queue(ns);
   };
   // one fast window: 32 vectors (128 waits) of one live, unserved queue range
-  auto fast_window = [&](const uint4 &x, uint32_t &carry) {
+  auto fast_window = [&](const uint4 &x, uint32_t &carry, bool qstart) {
     uint32_t prev = __shfl_up_sync(FULL, x.w, 1);
-    if (lane == 0) prev = carry;
+    if (lane == 0) prev = qstart ? 0xFFFFFFFFu : carry;  // no predecessor check at the queue head
     carry = __shfl_sync(FULL, x.w, 31);
     // Q24 read-window check as one predicate chain: bad = 1 if any wait exceeds its predecessor
     asm("{\n\t.reg .pred p;\n\t"
@@ -561,26 +578,45 @@ __global__ void __launch_bounds__(TMA_NW * 32, 1) k1s_stream_tma(const uint8_t *
     const int32_t pw0 = (int32_t)(4 * (vs - v0));
     for (uint32_t j = 0; j < nv; j += 32u) {  // windows of 32 vectors, warp-uniform
       const int32_t pw = pw0 + 4 * (int32_t)j;
+      while (qe_r <= pw) advance();  // queues that ended before this window (or are empty)
+      const bool qstart = pw == qs_r;
       if (pw >= lo_r && pw + 384 <= hi_r && j + 96u < nv) {  // four fast windows
         const uint32_t sa = sl + 16u * j;
         const uint4 x = lds_v4(sa), y = lds_v4(sa + 512u), z = lds_v4(sa + 1024u), u = lds_v4(sa + 1536u);
-        fast_window(x, carry);
-        fast_window(y, carry);
-        fast_window(z, carry);
-        fast_window(u, carry);
+        fast_window(x, carry, qstart);
+        fast_window(y, carry, false);
+        fast_window(z, carry, false);
+        fast_window(u, carry, false);
         j += 96u;
         continue;
       }
       if (pw >= lo_r && pw + 128 <= hi_r && j + 32u < nv) {  // two fast windows
         const uint4 x = lds_v4(sl + 16u * j), y = lds_v4(sl + 16u * (j + 32u));
-        fast_window(x, carry);
-        fast_window(y, carry);
+        fast_window(x, carry, qstart);
+        fast_window(y, carry, false);
         j += 32u;
         continue;
       }
       if (pw >= lo_r && pw <= hi_r) {
-        fast_window(lds_v4(sl + 16u * j), carry);
+        fast_window(lds_v4(sl + 16u * j), carry, qstart);
         continue;
+      }
+      // ---- one queue boundary inside the window, same snapshot (so the same
+      // SLO tables and slow flag), the next queue reaching past the window:
+      // every wait is summed into the snapshot total; the Q24 pair check skips
+      // only the next queue's head
+      if (pw >= lo_r && qe_r > pw && qe_r < pw + 128 && pw + 128 <= rend_full && m_cur + 1 < M &&
+          qi + 2 - qb <= 32 && clampr((int64_t)qoff(qi + 2)) >= pw + 128) {
+        const uint4 x = lds_v4(sl + 16u * j);
+        uint32_t prev = __shfl_up_sync(FULL, x.w, 1);
+        if (lane == 0) prev = carry;
+        carry = __shfl_sync(FULL, x.w, 31);
+        const int32_t pl = pw + 4 * lane;  // position of x.x
+        const bool inv = ((x.x > prev) & (pl != qe_r) & (pl != qs_r)) | ((x.y > x.x) & (pl + 1 != qe_r)) |
+                         ((x.z > x.y) & (pl + 2 != qe_r)) | ((x.w > x.z) & (pl + 3 != qe_r));
+        if (inv) bad = 1u;
+        tot += (uint64_t)Gv(x.x) + Gv(x.y) + (uint64_t)Gv(x.z) + Gv(x.w);
+        continue;  // the next window's catch-up advances to the next queue (same snapshot: no flush)
       }
       // ---- element-wise window: boundaries, served heads, skipped queues, range end
       const uint32_t vl = j + lane;

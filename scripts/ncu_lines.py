@@ -7,8 +7,9 @@ rep, ksub = sys.argv[1], sys.argv[2]
 top = int(sys.argv[3]) if len(sys.argv) > 3 else 40
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 lib = os.path.join(ROOT, "paper_2605_05527_b200", "libedgeserve.so")
-out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass"],
-                     capture_output=True, text=True).stdout
+kf = os.environ.get("KFILTER")  # ncu -k filter when the report holds several kernels
+out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass"] +
+                     (["-k", kf] if kf else []), capture_output=True, text=True).stdout
 rows = list(csv.reader(io.StringIO(out)))
 kname = rows[0][1]
 h = rows[1]
