@@ -63,13 +63,15 @@ struct StreamArgs {
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 
+// exact warp sum of u64 values whose total stays below 2^64 and whose high
+// words sum below 2^32: three REDUX (the low word split into 16-bit halves)
 __device__ __forceinline__ uint64_t wsum64_pre(uint64_t v) {
-#pragma unroll
-  for (int o = 16; o >= 1; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-  return v;
+  const uint32_t lo = (uint32_t)v, hi = (uint32_t)(v >> 32);
+  const uint64_t l0 = redux_add(lo & 0xFFFFu), l1 = redux_add(lo >> 16);
+  return l0 + (l1 << 16) + ((uint64_t)redux_add(hi) << 32);
 }
 
-__global__ void __launch_bounds__(256) k1s_prep(const uint8_t *__restrict__ gimg, ImgLayout lay, StreamArgs a) {
+__global__ void __launch_bounds__(256, 6) k1s_prep(const uint8_t *__restrict__ gimg, ImgLayout lay, StreamArgs a) {
   pdl_trigger();
   extern __shared__ __align__(16) uint8_t smem[];
   __shared__ uint64_t mbar;
