@@ -400,12 +400,15 @@ def main():
         if world > 1:
             dist.barrier()
         n_e2e = max(3, min(args.steps, 20))
+        # every step copies its own inputs in and its results out; the pipelined
+        # call overlaps step k+1's input copy with step k's replay
+        batches = [(*hin, ho) for _ in range(n_e2e)]
+        es.es_replay_traces_host_pipelined(h, batches[:2], stream=stream)
         a = time.perf_counter()
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
         e0.record(stream)
-        for _ in range(n_e2e):
-            es.es_replay_traces_host(h, *hin, out=ho, stream=stream)
+        es.es_replay_traces_host_pipelined(h, batches, stream=stream)
         e1.record(stream)
         torch.cuda.synchronize()
         e_ms = e0.elapsed_time(e1)
@@ -418,7 +421,9 @@ def main():
         d2h = int(ho["stats"].numel() * 8 + ho["p95"].numel() * 4)
         assert np.array_equal(ho["stats"].numpy(), st)
         line["e2e"] = {"value": e2e_v, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-                       "steps": n_e2e, "call": "es_replay_traces_host (pinned host in/out, K2+K3)"}
+                       "steps": n_e2e,
+                       "call": "es_replay_traces_host_pipelined (pinned host in/out per step, K2+K3; step k+1's "
+                               "H2D overlaps step k's replay)"}
 
     # ---------------- K1: independent snapshot scoring, the HBM-streaming form
     if not args.no_k1 and not args.ncu:

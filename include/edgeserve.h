@@ -262,6 +262,17 @@ ES_API es_status es_scen_p95(const es_profile *prof, const es_traces *traces, es
 ES_API es_status es_replay_traces_host(es_profile *prof, const es_traces *host_traces,
                                 es_replay_out *host_out, es_stream stream);
 
+/*
+ * Pipelined end-to-end replay of nbatch independent host batches (each with its
+ * own host traces and outputs, as in es_replay_traces_host): batch k's inputs
+ * are copied to one of two device buffers on a library-owned copy stream while
+ * batch k-1 replays on `stream`, so the host->device transfer overlaps the
+ * replay.  Every batch still moves its own inputs in and its outputs out.
+ * Synchronises `stream` before returning.  Errors as es_replay_traces_host.
+ */
+ES_API es_status es_replay_traces_host_pipelined(es_profile *prof, const es_traces *host_traces,
+                                          es_replay_out *host_outs, int32_t nbatch, es_stream stream);
+
 /* ------------------------------------------------ group merge (multi-GPU) */
 
 #define ES_NGSTAT 7 /* decisions, candidates, cells, completed, violations, infeasible, sum_lat */

@@ -30,6 +30,7 @@ STATUS = {0: "ES_OK", 1: "ES_ERR_ARG", 2: "ES_ERR_PROFILE_GRID", 3: "ES_ERR_PROF
           8: "ES_ERR_UNSORTED", 9: "ES_ERR_NUMERIC", 10: "ES_ERR_INTERNAL"}
 EXPORTS = ["es_last_error", "es_version", "es_load_profile", "es_free_profile", "es_get_tables",
            "es_score_candidates", "es_replay_traces", "es_scen_p95", "es_scen_stats", "es_replay_traces_host",
+           "es_replay_traces_host_pipelined",
            "es_group_accumulate",
            "es_group_hist", "es_group_p95_select", "es_device_status", "es_launch_count"]
 
@@ -94,6 +95,7 @@ def lib():
             "es_scen_p95": [P, P, P, P],
             "es_scen_stats": [P, P, P, u32, P, P, P],
             "es_replay_traces_host": [P, P, P, P],
+            "es_replay_traces_host_pipelined": [P, P, P, i32, P],
             "es_group_accumulate": [P, P, P, u32, P, P, P],
             "es_group_hist": [P, P, P, u32, i32, P, P, P],
             "es_group_p95_select": [u32, i32, P, P, P, P],
@@ -275,6 +277,21 @@ def es_replay_traces_host(prof: Profile, arr_off, arrival, cfg_idx=None, group_i
     ro = _out_struct(out)
     _check(lib().es_replay_traces_host(prof.handle, ctypes.byref(tr), ctypes.byref(ro), _stream(stream)))
     return out
+
+
+def es_replay_traces_host_pipelined(prof: Profile, batches, stream=None):
+    """End-to-end over several host batches, each (arr_off, arrival, cfg_idx,
+    group_id, out) with host (ideally pinned) arrays: the input copy of batch
+    k+1 overlaps the replay of batch k.  Returns the list of outs."""
+    nb = len(batches)
+    trs = (Traces * nb)()
+    ros = (ReplayOut * nb)()
+    for i, (arr_off, arrival, cfg_idx, group_id, out) in enumerate(batches):
+        n = (arr_off.numel() - 1) // prof.M if hasattr(arr_off, "numel") else (arr_off.size - 1) // prof.M
+        trs[i] = _traces_struct(n, arr_off, arrival, cfg_idx, group_id)
+        ros[i] = _out_struct(out)
+    _check(lib().es_replay_traces_host_pipelined(prof.handle, trs, ros, ctypes.c_int32(nb), _stream(stream)))
+    return [b[4] for b in batches]
 
 
 def es_group_accumulate(prof, arr_off, arrival, out, n_groups, counts, hist0, cfg_idx=None, group_id=None,

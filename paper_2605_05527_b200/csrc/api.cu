@@ -9,6 +9,7 @@
 #include <cuda_runtime.h>
 
 #include <cmath>
+#include <algorithm>
 #include <cstdarg>
 #include <cstdio>
 #include <cstdlib>
@@ -30,9 +31,13 @@ struct es_profile {
   std::vector<es_sched_cfg> cfgs;
   std::vector<uint8_t> h_img;  // host copy (after table build)
   int64_t launches = 0;
-  // scratch for es_replay_traces_host
+  // scratch for es_replay_traces_host (double-buffered by the pipelined call)
   uint8_t *scratch = nullptr;
   size_t scratch_bytes = 0;
+  uint8_t *scratch2 = nullptr;
+  size_t scratch2_bytes = 0;
+  cudaStream_t copy_stream = nullptr;
+  cudaEvent_t ev_copied[2] = {nullptr, nullptr}, ev_done[2] = {nullptr, nullptr}, ev_start = nullptr;
 };
 
 namespace {
@@ -257,6 +262,16 @@ es_status es_free_profile(es_profile *p) {
   cudaFree(p->d_status);
   cudaFree(p->d_work);
   cudaFree(p->scratch);
+  cudaFree(p->scratch2);
+  if (p->copy_stream) {
+    cudaStreamSynchronize(p->copy_stream);
+    cudaStreamDestroy(p->copy_stream);
+    for (int i = 0; i < 2; ++i) {
+      cudaEventDestroy(p->ev_copied[i]);
+      cudaEventDestroy(p->ev_done[i]);
+    }
+    cudaEventDestroy(p->ev_start);
+  }
   delete p;
   return ES_OK;
 }
@@ -337,56 +352,90 @@ es_status es_scen_p95(const es_profile *p, const es_traces *tr, es_replay_out *o
   return ES_OK;
 }
 
-es_status es_replay_traces_host(es_profile *p, const es_traces *ht, es_replay_out *ho, es_stream stream) {
-  if (!p || !ht || !ho) return fail(ES_ERR_ARG, "null argument");
-  if (ht->n_scen <= 0) return ht->n_scen == 0 ? ES_OK : fail(ES_ERR_ARG, "n_scen < 0");
-  if (!ht->arr_off || !ht->arrival_us || !ho->scen_stats) return fail(ES_ERR_ARG, "null host input/stats");
-  DeviceGuard guard(p->device);
-  cudaStream_t st = (cudaStream_t)stream;
+namespace {
+
+// device scratch layout of one host batch (es_replay_traces_host*)
+struct HostLayout {
+  size_t b_off, b_arr, b_cfg, b_grp, b_comp, b_exit, b_lat, b_st, b_p95, b_dec;
+  size_t o_off, o_arr, o_cfg, o_grp, o_comp, o_exit, o_lat, o_st, o_p95, o_dec;
+  size_t need;
+  int64_t dc;
+};
+
+HostLayout host_layout(const es_profile *p, const es_traces *ht, const es_replay_out *ho) {
+  HostLayout L{};
   const int M = p->lay.M;
   const int64_t n = ht->n_scen;
   const uint64_t total = ht->arr_off[n * M];
-  const size_t b_off = 8u * (size_t)(n * M + 1), b_arr = 4u * total, b_cfg = ht->cfg_idx ? 2u * n : 0,
-               b_grp = ht->group_id ? 4u * n : 0, b_comp = ho->completion_us ? 4u * total : 0,
-               b_exit = ho->exit_used ? total : 0, b_lat = 4u * total, b_st = 8u * ES_NSTAT * n,
-               b_p95 = ho->scen_p95_us ? 4u * n : 0;
-  const int64_t dc = ho->dec_cap;
-  const size_t b_dec = dc > 0 ? (size_t)(n * dc) * (4 + 1 + 1 + 2 + 4 + 8 + 1) : 0;
+  L.b_off = 8u * (size_t)(n * M + 1);
+  L.b_arr = 4u * total;
+  L.b_cfg = ht->cfg_idx ? 2u * n : 0;
+  L.b_grp = ht->group_id ? 4u * n : 0;
+  L.b_comp = ho->completion_us ? 4u * total : 0;
+  L.b_exit = ho->exit_used ? total : 0;
+  L.b_lat = 4u * total;
+  L.b_st = 8u * ES_NSTAT * n;
+  L.b_p95 = ho->scen_p95_us ? 4u * n : 0;
+  L.dc = ho->dec_cap;
+  L.b_dec = L.dc > 0 ? (size_t)(n * L.dc) * (4 + 1 + 1 + 2 + 4 + 8 + 1) : 0;
   size_t need = 0;
   auto take = [&](size_t b) {
     size_t o = need;
     need += (b + 255) & ~(size_t)255;
     return o;
   };
-  const size_t o_off = take(b_off), o_arr = take(b_arr), o_cfg = take(b_cfg), o_grp = take(b_grp),
-               o_comp = take(b_comp), o_exit = take(b_exit), o_lat = take(b_lat), o_st = take(b_st),
-               o_p95 = take(b_p95), o_dec = take(b_dec);
-  if (need > p->scratch_bytes) {
-    cudaFree(p->scratch);
-    p->scratch = nullptr;
-    p->scratch_bytes = 0;
-    CK(cudaMalloc(&p->scratch, need), "cudaMalloc(scratch)");
-    p->scratch_bytes = need;
-  }
-  uint8_t *S = p->scratch;
-  CK(cudaMemcpyAsync(S + o_off, ht->arr_off, b_off, cudaMemcpyHostToDevice, st), "H2D arr_off");
-  CK(cudaMemcpyAsync(S + o_arr, ht->arrival_us, b_arr, cudaMemcpyHostToDevice, st), "H2D arrival");
-  if (b_cfg) CK(cudaMemcpyAsync(S + o_cfg, ht->cfg_idx, b_cfg, cudaMemcpyHostToDevice, st), "H2D cfg_idx");
-  if (b_grp) CK(cudaMemcpyAsync(S + o_grp, ht->group_id, b_grp, cudaMemcpyHostToDevice, st), "H2D group_id");
+  L.o_off = take(L.b_off);
+  L.o_arr = take(L.b_arr);
+  L.o_cfg = take(L.b_cfg);
+  L.o_grp = take(L.b_grp);
+  L.o_comp = take(L.b_comp);
+  L.o_exit = take(L.b_exit);
+  L.o_lat = take(L.b_lat);
+  L.o_st = take(L.b_st);
+  L.o_p95 = take(L.b_p95);
+  L.o_dec = take(L.b_dec);
+  L.need = need;
+  return L;
+}
+
+es_status ensure_buf(uint8_t **buf, size_t *bytes, size_t need) {
+  if (need <= *bytes) return ES_OK;
+  cudaFree(*buf);
+  *buf = nullptr;
+  *bytes = 0;
+  CK(cudaMalloc(buf, need), "cudaMalloc(scratch)");
+  *bytes = need;
+  return ES_OK;
+}
+
+// host -> device copies of one batch's inputs into scratch S
+es_status host_in(const HostLayout &L, const es_traces *ht, uint8_t *S, cudaStream_t st) {
+  CK(cudaMemcpyAsync(S + L.o_off, ht->arr_off, L.b_off, cudaMemcpyHostToDevice, st), "H2D arr_off");
+  CK(cudaMemcpyAsync(S + L.o_arr, ht->arrival_us, L.b_arr, cudaMemcpyHostToDevice, st), "H2D arrival");
+  if (L.b_cfg) CK(cudaMemcpyAsync(S + L.o_cfg, ht->cfg_idx, L.b_cfg, cudaMemcpyHostToDevice, st), "H2D cfg_idx");
+  if (L.b_grp) CK(cudaMemcpyAsync(S + L.o_grp, ht->group_id, L.b_grp, cudaMemcpyHostToDevice, st), "H2D group_id");
+  return ES_OK;
+}
+
+// K2 + K3 on the batch in scratch S, then device -> host copies of its outputs
+es_status host_run(const es_profile *p, const HostLayout &L, const es_traces *ht, es_replay_out *ho, uint8_t *S,
+                   cudaStream_t st) {
   es_traces dt = *ht;
-  dt.arr_off = reinterpret_cast<const uint64_t *>(S + o_off);
-  dt.arrival_us = reinterpret_cast<const uint32_t *>(S + o_arr);
-  dt.cfg_idx = b_cfg ? reinterpret_cast<const uint16_t *>(S + o_cfg) : nullptr;
-  dt.group_id = b_grp ? reinterpret_cast<const uint32_t *>(S + o_grp) : nullptr;
+  dt.arr_off = reinterpret_cast<const uint64_t *>(S + L.o_off);
+  dt.arrival_us = reinterpret_cast<const uint32_t *>(S + L.o_arr);
+  dt.cfg_idx = L.b_cfg ? reinterpret_cast<const uint16_t *>(S + L.o_cfg) : nullptr;
+  dt.group_id = L.b_grp ? reinterpret_cast<const uint32_t *>(S + L.o_grp) : nullptr;
   es_replay_out dout{};
-  dout.completion_us = b_comp ? reinterpret_cast<uint32_t *>(S + o_comp) : nullptr;
-  dout.exit_used = b_exit ? S + o_exit : nullptr;
-  dout.latency_us = reinterpret_cast<uint32_t *>(S + o_lat);
-  dout.scen_stats = reinterpret_cast<uint64_t *>(S + o_st);
-  dout.scen_p95_us = b_p95 ? reinterpret_cast<uint32_t *>(S + o_p95) : nullptr;
+  dout.completion_us = L.b_comp ? reinterpret_cast<uint32_t *>(S + L.o_comp) : nullptr;
+  dout.exit_used = L.b_exit ? S + L.o_exit : nullptr;
+  dout.latency_us = reinterpret_cast<uint32_t *>(S + L.o_lat);
+  dout.scen_stats = reinterpret_cast<uint64_t *>(S + L.o_st);
+  dout.scen_p95_us = L.b_p95 ? reinterpret_cast<uint32_t *>(S + L.o_p95) : nullptr;
+  const int64_t dc = L.dc;
+  const int64_t n = ht->n_scen;
   dout.dec_cap = dc > 0 ? dc : 0;
   if (dc > 0) {
-    uint8_t *q = S + o_dec;
+    uint8_t *q = S + L.o_dec;
     const size_t nd = (size_t)(n * dc);
     dout.dec_t_us = reinterpret_cast<uint32_t *>(q);
     q += 4 * nd;
@@ -402,13 +451,15 @@ es_status es_replay_traces_host(es_profile *p, const es_traces *ht, es_replay_ou
     q += nd;
     dout.dec_flags = q;
   }
-  es_status s = es_replay_traces(p, &dt, &dout, stream);
+  es_status s = es_replay_traces(p, &dt, &dout, (es_stream)st);
   if (s) return s;
-  CK(cudaMemcpyAsync(ho->scen_stats, dout.scen_stats, b_st, cudaMemcpyDeviceToHost, st), "D2H stats");
-  if (b_p95) CK(cudaMemcpyAsync(ho->scen_p95_us, dout.scen_p95_us, b_p95, cudaMemcpyDeviceToHost, st), "D2H p95");
-  if (ho->latency_us) CK(cudaMemcpyAsync(ho->latency_us, dout.latency_us, b_lat, cudaMemcpyDeviceToHost, st), "D2H lat");
-  if (b_comp) CK(cudaMemcpyAsync(ho->completion_us, dout.completion_us, b_comp, cudaMemcpyDeviceToHost, st), "D2H comp");
-  if (b_exit) CK(cudaMemcpyAsync(ho->exit_used, dout.exit_used, b_exit, cudaMemcpyDeviceToHost, st), "D2H exit");
+  CK(cudaMemcpyAsync(ho->scen_stats, dout.scen_stats, L.b_st, cudaMemcpyDeviceToHost, st), "D2H stats");
+  if (L.b_p95) CK(cudaMemcpyAsync(ho->scen_p95_us, dout.scen_p95_us, L.b_p95, cudaMemcpyDeviceToHost, st), "D2H p95");
+  if (ho->latency_us)
+    CK(cudaMemcpyAsync(ho->latency_us, dout.latency_us, L.b_lat, cudaMemcpyDeviceToHost, st), "D2H lat");
+  if (L.b_comp)
+    CK(cudaMemcpyAsync(ho->completion_us, dout.completion_us, L.b_comp, cudaMemcpyDeviceToHost, st), "D2H comp");
+  if (L.b_exit) CK(cudaMemcpyAsync(ho->exit_used, dout.exit_used, L.b_exit, cudaMemcpyDeviceToHost, st), "D2H exit");
   if (dc > 0) {
     const size_t nd = (size_t)(n * dc);
     if (ho->dec_t_us) CK(cudaMemcpyAsync(ho->dec_t_us, dout.dec_t_us, 4 * nd, cudaMemcpyDeviceToHost, st), "D2H dec");
@@ -419,6 +470,75 @@ es_status es_replay_traces_host(es_profile *p, const es_traces *ht, es_replay_ou
     if (ho->dec_m) CK(cudaMemcpyAsync(ho->dec_m, dout.dec_m, nd, cudaMemcpyDeviceToHost, st), "D2H dec");
     if (ho->dec_e) CK(cudaMemcpyAsync(ho->dec_e, dout.dec_e, nd, cudaMemcpyDeviceToHost, st), "D2H dec");
     if (ho->dec_flags) CK(cudaMemcpyAsync(ho->dec_flags, dout.dec_flags, nd, cudaMemcpyDeviceToHost, st), "D2H dec");
+  }
+  return ES_OK;
+}
+
+es_status check_host_batch(const es_traces *ht, const es_replay_out *ho) {
+  if (!ht || !ho) return fail(ES_ERR_ARG, "null argument");
+  if (ht->n_scen < 0) return fail(ES_ERR_ARG, "n_scen < 0");
+  if (ht->n_scen > 0 && (!ht->arr_off || !ht->arrival_us || !ho->scen_stats))
+    return fail(ES_ERR_ARG, "null host input/stats");
+  return ES_OK;
+}
+
+}  // namespace
+
+es_status es_replay_traces_host(es_profile *p, const es_traces *ht, es_replay_out *ho, es_stream stream) {
+  if (!p) return fail(ES_ERR_ARG, "null argument");
+  es_status s = check_host_batch(ht, ho);
+  if (s) return s;
+  if (ht->n_scen == 0) return ES_OK;
+  DeviceGuard guard(p->device);
+  cudaStream_t st = (cudaStream_t)stream;
+  const HostLayout L = host_layout(p, ht, ho);
+  if ((s = ensure_buf(&p->scratch, &p->scratch_bytes, L.need))) return s;
+  if ((s = host_in(L, ht, p->scratch, st))) return s;
+  if ((s = host_run(p, L, ht, ho, p->scratch, st))) return s;
+  CK(cudaStreamSynchronize(st), "stream sync");
+  return ES_OK;
+}
+
+es_status es_replay_traces_host_pipelined(es_profile *p, const es_traces *hts, es_replay_out *hos, int32_t nbatch,
+                                          es_stream stream) {
+  if (!p || !hts || !hos || nbatch < 0) return fail(ES_ERR_ARG, "null argument or nbatch < 0");
+  size_t need = 0;
+  for (int32_t k = 0; k < nbatch; ++k) {
+    es_status s = check_host_batch(&hts[k], &hos[k]);
+    if (s) return s;
+    if (hts[k].n_scen > 0) need = std::max(need, host_layout(p, &hts[k], &hos[k]).need);
+  }
+  if (need == 0) return ES_OK;
+  DeviceGuard guard(p->device);
+  cudaStream_t st = (cudaStream_t)stream;
+  es_status s;
+  if ((s = ensure_buf(&p->scratch, &p->scratch_bytes, need))) return s;
+  if ((s = ensure_buf(&p->scratch2, &p->scratch2_bytes, need))) return s;
+  if (!p->copy_stream) {
+    CK(cudaStreamCreateWithFlags(&p->copy_stream, cudaStreamNonBlocking), "copy stream");
+    for (int i = 0; i < 2; ++i) {
+      CK(cudaEventCreateWithFlags(&p->ev_copied[i], cudaEventDisableTiming), "event");
+      CK(cudaEventCreateWithFlags(&p->ev_done[i], cudaEventDisableTiming), "event");
+    }
+    CK(cudaEventCreateWithFlags(&p->ev_start, cudaEventDisableTiming), "event");
+  }
+  // the copy stream starts after the caller's prior work on `stream`
+  CK(cudaEventRecord(p->ev_start, st), "event record");
+  CK(cudaStreamWaitEvent(p->copy_stream, p->ev_start, 0), "stream wait");
+  // batch k: inputs into buffer k % 2 on the copy stream (after batch k-2 is
+  // done with it), K2 + K3 + output copies on `stream` after its inputs landed:
+  // the input copy of batch k+1 overlaps the replay of batch k
+  for (int32_t k = 0; k < nbatch; ++k) {
+    if (hts[k].n_scen == 0) continue;
+    const int b = k & 1;
+    uint8_t *S = b ? p->scratch2 : p->scratch;
+    const HostLayout L = host_layout(p, &hts[k], &hos[k]);
+    if (k >= 2) CK(cudaStreamWaitEvent(p->copy_stream, p->ev_done[b], 0), "stream wait");
+    if ((s = host_in(L, &hts[k], S, p->copy_stream))) return s;
+    CK(cudaEventRecord(p->ev_copied[b], p->copy_stream), "event record");
+    CK(cudaStreamWaitEvent(st, p->ev_copied[b], 0), "stream wait");
+    if ((s = host_run(p, L, &hts[k], &hos[k], S, st))) return s;
+    CK(cudaEventRecord(p->ev_done[b], st), "event record");
   }
   CK(cudaStreamSynchronize(st), "stream sync");
   return ES_OK;

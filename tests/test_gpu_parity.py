@@ -304,6 +304,28 @@ def test_host_entry_point_matches_device():
     assert_k2_equal(g, o)
 
 
+def test_host_pipelined_batches_match_oracle():
+    """es_replay_traces_host_pipelined: five batches of different sizes and
+    configs through the double-buffered pipeline (input copy of batch k+1
+    overlapping the replay of batch k); every batch equals the oracle."""
+    pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory()
+    w0 = inputs.workload("cfg2", scen_ids=np.arange(3), n_req=500)
+    h = es.es_load_profile(w0.profile, w0.cfgs)
+    batches, refs = [], []
+    for k, ids in enumerate([np.arange(20), np.arange(40, 47), np.arange(100, 160), np.arange(5), np.arange(7, 30)]):
+        w = inputs.workload("cfg2", scen_ids=ids, n_req=800 + 200 * k)
+        tr = w.traces
+        total = tr.arrival.size
+        ho = {"latency": pin(np.zeros(total, np.uint32)), "stats": pin(np.zeros((tr.n_scen, es.ES_NSTAT), np.uint64)),
+              "p95": pin(np.zeros(tr.n_scen, np.uint32)), "completion": pin(np.zeros(total, np.uint32)),
+              "exit": pin(np.zeros(total, np.uint8)), "dec_cap": 0}
+        batches.append((pin(tr.arr_off), pin(tr.arrival), pin(tr.cfg_idx), pin(tr.group_id), ho))
+        refs.append(oracle.replay_batch(w.profile, w.cfgs, tr, nthreads=4))
+    es.es_replay_traces_host_pipelined(h, batches)
+    for (_, _, _, _, ho), o in zip(batches, refs):
+        assert_k2_equal({k: (v.numpy() if hasattr(v, "numpy") else v) for k, v in ho.items()}, o)
+
+
 def test_full_size_cfg2_bench_config():
     """BASELINE configs[1] at full size in the bench's launch configuration:
     every scenario's counters and P95 against the oracle (16 host threads),
