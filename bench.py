@@ -169,7 +169,7 @@ def alg_ops(stats_sum, requests, E):
     return 3 * terms + 7 * live + 2 * cells + 7 * c + 4 * requests + 2 * d
 
 
-def k1_batch(rank, n_gen=4096, tiles=16, depth=4096):
+def k1_batch(rank, n_gen=4096, tiles=64, depth=4096):
     """The K1 bench batch (host arrays): n_gen distinct seeded 5-C snapshots
     (inputs.snapshots_poisson_depth), repeated `tiles` times back to back in
     the flat CSR layout (snapshots are scored independently; the repetition
@@ -187,8 +187,8 @@ def bench_k1(es, h_cache, dev, stream, rank, depth=4096, iters=10):
     """K1 (es_score_candidates) on 5-C-shaped snapshots: M=8, E=5, batch 1-32,
     per-model depth U[0, 4096], waits = t - Poisson arrivals in FIFO order.
     Rates are set so a full queue spans ~120 ms < x_c - max L: every task is in
-    the live window and is read (the HBM-streaming regime).  65,536 snapshots
-    (4.3 GB of waits, a quarter of 5-C's 262,144; k1_batch).
+    the live window and is read (the HBM-streaming regime).  262,144 snapshots
+    (17.3 GB of waits: SURVEY 5-C's full size; k1_batch).
     Timed per launch with CUDA events, L2 flushed between launches."""
     import torch
     import inputs

@@ -442,7 +442,7 @@ def test_k1_all_mappings(monkeypatch, mode):
 
 def test_k1_full_size_bench_batch():
     """K1 at the bench's full size and launch configuration (bench.k1_batch:
-    65,536 5-C snapshots, 4.3 GB of waits, the TMA stream mapping): 512
+    262,144 5-C snapshots, 17.3 GB of waits, the TMA stream mapping): 512
     sampled snapshots spread over every tile against the oracle, element by
     element, plus properties that hold for every snapshot (Eq. 7's choice is
     the argmin of the candidate scores, Q3 tie-break)."""
