@@ -26,6 +26,7 @@
 // primitive is executed by the whole warp.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdlib>
 
 #include "decide.cuh"
@@ -51,6 +52,7 @@ struct ReplayArgs {
   uint8_t *dec_f;
   DevStatus *dstat;
   unsigned long long *work;
+  const uint32_t *order;  // scenario hand-out order (longest traces first), or null
   bool any_simple;  // some cfg selects by LQF / EDF / deferred batching (Q26, Q27)
   bool any_score;   // some cfg selects by the stability score (Eq. 7)
   bool any_grid;    // some cfg scores every (m, e, b) cell (f2, Q28)
@@ -123,7 +125,7 @@ __global__ void __launch_bounds__(256) k2_replay(const uint8_t *__restrict__ gim
       int k = 0;
       uint32_t n_new = 0, a0 = 0xFFFFFFFFu;
       if (fresh) {
-        s = (int64_t)got;
+        s = a.order ? (int64_t)a.order[got] : (int64_t)got;
         k = a.cfg_idx ? (int)a.cfg_idx[s] : 0;
         qb = 0;
         if (k < P.ncfg) {
@@ -341,6 +343,56 @@ __global__ void __launch_bounds__(256) k2_replay(const uint8_t *__restrict__ gim
   }
 }
 
+// ---- hand-out order: K2's time is its longest chain, so the segments pick up
+// the scenarios in decreasing order of trace span (last - first arrival; at a
+// fixed request count a longer span means lighter load, smaller batches, more
+// decisions) -- longest-processing-time-first.  64 span buckets (counting
+// sort); the order inside a bucket is arbitrary.  Results do not depend on it
+// (scenarios are independent and write fixed slots).
+constexpr int NBK = 64;
+
+__global__ void k2_order_span(int64_t n_scen, int M, const uint64_t *__restrict__ arr_off,
+                              const uint32_t *__restrict__ arrival, uint32_t *span, unsigned *sc) {
+  for (int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; s < n_scen; s += (int64_t)gridDim.x * blockDim.x) {
+    uint32_t lo = 0xFFFFFFFFu, hi = 0u;
+    for (int m = 0; m < M; ++m) {
+      const uint64_t b = arr_off[s * M + m], e = arr_off[s * M + m + 1];
+      if (e > b) {
+        lo = min(lo, __ldg(arrival + b));
+        hi = max(hi, __ldg(arrival + e - 1));
+      }
+    }
+    const uint32_t v = hi >= lo ? hi - lo : 0u;
+    span[s] = v;
+    atomicMax(sc, v);
+  }
+}
+
+__global__ void k2_order_hist(int64_t n_scen, const uint32_t *span, unsigned *sc) {
+  const uint64_t mx = (uint64_t)sc[0] + 1u;
+  for (int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; s < n_scen; s += (int64_t)gridDim.x * blockDim.x) {
+    const int b = NBK - 1 - (int)((uint64_t)span[s] * NBK / mx);  // longest spans -> bucket 0
+    atomicAdd(sc + 1 + b, 1u);
+  }
+}
+
+__global__ void k2_order_scatter(int64_t n_scen, const uint32_t *span, unsigned *sc, uint32_t *order) {
+  __shared__ unsigned base[NBK];
+  if (threadIdx.x == 0) {
+    unsigned acc = 0;
+    for (int b = 0; b < NBK; ++b) {
+      base[b] = acc;
+      acc += sc[1 + b];
+    }
+  }
+  __syncthreads();
+  const uint64_t mx = (uint64_t)sc[0] + 1u;
+  for (int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; s < n_scen; s += (int64_t)gridDim.x * blockDim.x) {
+    const int b = NBK - 1 - (int)((uint64_t)span[s] * NBK / mx);
+    order[base[b] + atomicAdd(sc + 1 + NBK + b, 1u)] = (uint32_t)s;
+  }
+}
+
 template <int LPS, int MM>
 cudaError_t launch_t(const uint8_t *img, const ImgLayout &lay, const ReplayArgs &a, cudaStream_t st, int sms) {
   // Algorithm 1 alone compiles without the policy code (no cost on the bench path)
@@ -408,6 +460,7 @@ cudaError_t launch_replay(const uint8_t *img, const ImgLayout &lay, const es_tra
   a.dec_f = out.dec_flags;
   a.dstat = dstat;
   a.work = reinterpret_cast<unsigned long long *>(work_ctr);
+  a.order = nullptr;
   constexpr uint32_t SCORE_POLS =
       (1u << ES_POLICY_EDGESERVING) | (1u << ES_POLICY_ALLFINAL_DA) | (1u << ES_POLICY_OURS_BS1);
   constexpr uint32_t GRID_POLS = 1u << ES_POLICY_GRID;
@@ -417,10 +470,34 @@ cudaError_t launch_replay(const uint8_t *img, const ImgLayout &lay, const es_tra
   cudaError_t e = cudaMemsetAsync(work_ctr, 0, sizeof(unsigned long long), st);
   if (e != cudaSuccess) return e;
   *n_launch += 1;
+  // longest-span-first hand-out order (ES_K2_ORDER=0: scenario index order)
+  void *ord = nullptr;
+  const char *oe = getenv("ES_K2_ORDER");
+  if (tr.n_scen > 1 && tr.n_scen < (int64_t)0xFFFFFFFF && !(oe && oe[0] == '0')) {
+    const size_t ob = 4u * (size_t)tr.n_scen, sb = 4u * (1 + 2 * NBK);
+    e = cudaMallocAsync(&ord, 2 * ob + sb, st);
+    if (e != cudaSuccess) return e;
+    uint32_t *order = static_cast<uint32_t *>(ord), *span = order + tr.n_scen;
+    unsigned *sc = reinterpret_cast<unsigned *>(span + tr.n_scen);
+    e = cudaMemsetAsync(sc, 0, sb, st);
+    const int blocks = (int)std::min<int64_t>((tr.n_scen + 255) / 256, (int64_t)sms * 8);
+    if (e == cudaSuccess) k2_order_span<<<blocks, 256, 0, st>>>(tr.n_scen, lay.M, tr.arr_off, tr.arrival_us, span, sc);
+    if (e == cudaSuccess) k2_order_hist<<<blocks, 256, 0, st>>>(tr.n_scen, span, sc);
+    if (e == cudaSuccess) k2_order_scatter<<<blocks, 256, 0, st>>>(tr.n_scen, span, sc, order);
+    if (e == cudaSuccess) e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    a.order = order;
+    *n_launch += 3;
+  }
   const int lps = choose_lps(lay);
-  if (lps == 8 && lay.M <= 8) return launch_lps<8>(img, lay, a, st, sms);
-  if (lps == 16) return launch_lps<16>(img, lay, a, st, sms);
-  return launch_lps<32>(img, lay, a, st, sms);
+  e = lps == 8 && lay.M <= 8 ? launch_lps<8>(img, lay, a, st, sms)
+      : lps == 16            ? launch_lps<16>(img, lay, a, st, sms)
+                             : launch_lps<32>(img, lay, a, st, sms);
+  if (ord) {
+    const cudaError_t f = cudaFreeAsync(ord, st);
+    if (e == cudaSuccess) e = f;
+  }
+  return e;
 }
 
 }  // namespace es
