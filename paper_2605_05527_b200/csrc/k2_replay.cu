@@ -399,19 +399,36 @@ cudaError_t launch_t(const uint8_t *img, const ImgLayout &lay, const ReplayArgs 
   auto kern = lay.pol_mask == (1u << ES_POLICY_EDGESERVING) ? k2_replay<LPS, MM, false> : k2_replay<LPS, MM, true>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lay.bytes);
   if (e != cudaSuccess) return e;
-  // threads per block (ES_K2_BLOCK = 64 / 128 / 256): smaller blocks spread the
-  // scenarios' warps more evenly over the SMs when there is < 1 wave of them
+  // threads per block: the smallest of 64 / 128 / 256 that keeps the resident
+  // thread count of 256-thread blocks (small blocks deal the longest-first
+  // scenarios round-robin over the SMs in finer grains; a large profile image
+  // -- one CTA per SM by shared memory -- keeps 256).  ES_K2_BLOCK overrides.
+  int occ = 0;
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 256, lay.bytes);
+  if (e != cudaSuccess) return e;
   int threads = 256;
+  for (int t = 64; t < 256; t *= 2) {
+    int o = 0;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, kern, t, lay.bytes);
+    if (e != cudaSuccess) return e;
+    if (o * t >= occ * 256) {
+      threads = t;
+      occ = o;
+      break;
+    }
+  }
   if (const char *env = getenv("ES_K2_BLOCK")) {
     const int v = atoi(env);
-    if (v == 64 || v == 128 || v == 256) threads = v;
+    if (v == 32 || v == 64 || v == 128 || v == 256) {
+      threads = v;
+      e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, threads, lay.bytes);
+      if (e != cudaSuccess) return e;
+    }
   }
-  int occ = 0;
-  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, threads, lay.bytes);
-  if (e != cudaSuccess) return e;
   if (occ < 1) return cudaErrorInvalidConfiguration;
   const int seg_per_block = threads / LPS;
   int64_t blocks = (a.n_scen + seg_per_block - 1) / seg_per_block;
+  if (const char *env = getenv("ES_K2_OCC")) occ = std::max(1, std::min(occ, atoi(env)));  // resident CTAs/SM cap
   const int64_t cap = (int64_t)sms * occ;
   if (blocks > cap) blocks = cap;
   if (blocks < 1) blocks = 1;
