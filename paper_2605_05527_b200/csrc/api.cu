@@ -178,11 +178,17 @@ es_status es_load_profile(const es_profile_desc *desc, const es_sched_cfg *cfgs,
     off = align16(off + 4u * r.nA_cap);
     r.off_Bt = off;
     off = align16(off + 4u * 1024u);
-    r.off_H = off;
-    off = align16(off + 8u * cells);
     r.off_bidx = off;
     off = align16(off + r.b_max + 1u);
     r.status = 0xFFFFFFFFu;
+  }
+  // the H tables of every cfg at the tail: kernels that need the urgency
+  // tables in shared memory but can read H (one load per candidate) from
+  // global memory stage only [0, core_bytes)
+  lay.core_bytes = off;
+  for (int k = 0; k < ncfg; ++k) {
+    recs[k].off_H = off;
+    off = align16(off + 8u * cells);
   }
   lay.bytes = off;
   lay.pol_mask = 0;

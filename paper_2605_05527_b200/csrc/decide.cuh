@@ -50,6 +50,7 @@ __device__ __forceinline__ bool policy_scores(uint32_t pol) {
 
 struct SmemProf {
   const uint8_t *sm;
+  const uint8_t *hb;  // base of the H tables: the staged image, or the global one (core-only staging)
   const uint32_t *lat;
   const uint16_t *bs;
   const uint32_t *mask;
@@ -60,6 +61,7 @@ struct SmemProf {
 __device__ __forceinline__ SmemProf smem_prof(const uint8_t *sm, const ImgLayout &lay) {
   SmemProf p;
   p.sm = sm;
+  p.hb = sm;
   p.lat = reinterpret_cast<const uint32_t *>(sm + lay.off_lat);
   p.bs = reinterpret_cast<const uint16_t *>(sm + lay.off_bs);
   p.mask = reinterpret_cast<const uint32_t *>(sm + lay.off_mask);
@@ -275,7 +277,7 @@ __device__ __forceinline__ Cand cand_params(const Seg<LPS, MM> &sg, const SmemPr
   if (P.E <= GL) {  // warp-uniform: one exit per lane, L and H fetched in parallel
     const int e = sg.gl < P.E ? sg.gl : 0;
     const uint32_t Le = row[e * P.nb];
-    const uint64_t He = reinterpret_cast<const uint64_t *>(P.sm + C.off_H)[((size_t)gg * P.E + e) * P.nb + bi];
+    const uint64_t He = reinterpret_cast<const uint64_t *>(P.hb + C.off_H)[((size_t)gg * P.E + e) * P.nb + bi];
     const bool ok = sg.gl < P.E && ((mbits >> sg.gl) & 1u) && (uint64_t)wmax + Le <= (uint64_t)C.tau;
     bits = sg.gbits(__ballot_sync(FULL, ok));
     k.feas = bits != 0u;
@@ -303,7 +305,7 @@ __device__ __forceinline__ Cand cand_params(const Seg<LPS, MM> &sg, const SmemPr
   k.L = row[k.e * P.nb];
   if (fixed) k.feas = (uint64_t)wmax + k.L <= (uint64_t)C.tau;
   k.thr = k.L < C.x_c ? C.x_c - k.L : 0u;
-  k.H = k.L < C.x_c ? reinterpret_cast<const uint64_t *>(P.sm + C.off_H)[((size_t)gg * P.E + k.e) * P.nb + bi]
+  k.H = k.L < C.x_c ? reinterpret_cast<const uint64_t *>(P.hb + C.off_H)[((size_t)gg * P.E + k.e) * P.nb + bi]
                     : 0ull;
   return k;
 }
@@ -418,7 +420,7 @@ __device__ __noinline__ Decision decide_grid(const Seg<LPS, MM> &sg, const SmemP
   bool bfeas = false;
   ncells = 0u;
   const uint32_t cpre = sg.sum(sg.gl == 0 ? c : 0u);
-  const uint64_t *Hq = reinterpret_cast<const uint64_t *>(P.sm + C.off_H);
+  const uint64_t *Hq = reinterpret_cast<const uint64_t *>(P.hb + C.off_H);
   for (int m = 0; m < P.M; ++m) {
     const uint32_t len_m = sg.bcast(len, m * GL), c_m = sg.bcast(c, m * GL), wmax_m = sg.bcast(wmax, m * GL);
     const uint32_t cap = len_m < C.b_max ? len_m : C.b_max;

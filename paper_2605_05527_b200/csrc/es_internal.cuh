@@ -35,7 +35,8 @@ struct __align__(16) CfgRec {
 static_assert(sizeof(CfgRec) == 80, "CfgRec layout");
 
 struct ImgLayout {
-  uint32_t bytes;  // total, multiple of 16
+  uint32_t bytes;       // total, multiple of 16
+  uint32_t core_bytes;  // prefix without the per-cfg H tables (they form the tail)
   int32_t M, E, nb, ncfg;
   uint32_t off_lat, off_bs, off_mask, off_cfg;
   // cfg 0's urgency-table constants (host-computed), kernel parameters for the

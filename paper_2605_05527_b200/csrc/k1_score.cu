@@ -232,7 +232,7 @@ __global__ void __launch_bounds__(BT) k1_block(const uint8_t *__restrict__ gimg,
       s_L[tid] = L;
       s_feas[tid] = best >= 0;
       s_thr[tid] = L < C.x_c ? C.x_c - L : 0u;
-      s_H[tid] = L < C.x_c ? reinterpret_cast<const uint64_t *>(P.sm + C.off_H)[((size_t)tid * P.E + e) * P.nb + bi]
+      s_H[tid] = L < C.x_c ? reinterpret_cast<const uint64_t *>(P.hb + C.off_H)[((size_t)tid * P.E + e) * P.nb + bi]
                            : 0ull;
       if (s_wmax[tid] >= C.fast_lim) s_fast = 0;
     }

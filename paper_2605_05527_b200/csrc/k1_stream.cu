@@ -121,7 +121,7 @@ __global__ void __launch_bounds__(256, 6) k1s_prep(const uint8_t *__restrict__ g
       r.L = row[e * P.nb];
       r.ef = e | (best >= 0 ? 0x80u : 0u);
       r.thr = r.L < C.x_c ? C.x_c - r.L : 0u;
-      r.H = r.L < C.x_c ? reinterpret_cast<const uint64_t *>(P.sm + C.off_H)[((size_t)g * P.E + e) * P.nb + bi] : 0ull;
+      r.H = r.L < C.x_c ? reinterpret_cast<const uint64_t *>(P.hb + C.off_H)[((size_t)g * P.E + e) * P.nb + bi] : 0ull;
       nsv = r.B < r.len ? r.B : r.len;
       if (wmax >= C.fast_lim || C.x_c > V4_LIM) {
         const unsigned long long was = atomicOr(a.acc + s * ACC + 1, F_SLOW);

@@ -236,7 +236,7 @@ __global__ void __launch_bounds__(256) k2_lane(const uint8_t *__restrict__ gimg,
         e = feas ? (uint32_t)best : e_shallow;
         L = row[e * P.nb];
         thr = L < C.x_c ? C.x_c - L : 0u;
-        H = L < C.x_c ? reinterpret_cast<const uint64_t *>(P.sm + C.off_H)[((size_t)g * P.E + e) * P.nb + bi] : 0ull;
+        H = L < C.x_c ? reinterpret_cast<const uint64_t *>(P.hb + C.off_H)[((size_t)g * P.E + e) * P.nb + bi] : 0ull;
       }
       // ---- a5/a6: stability score of every candidate (Eq. 3-4, reading Q5)
       const uint32_t tt = t;

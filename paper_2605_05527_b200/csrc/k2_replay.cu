@@ -53,6 +53,7 @@ struct ReplayArgs {
   DevStatus *dstat;
   unsigned long long *work;
   const uint32_t *order;  // scenario hand-out order (longest traces first), or null
+  uint32_t stage_bytes;   // image bytes staged in shared memory (core only: H read from global)
   bool any_simple;  // some cfg selects by LQF / EDF / deferred batching (Q26, Q27)
   bool any_score;   // some cfg selects by the stability score (Eq. 7)
   bool any_grid;    // some cfg scores every (m, e, b) cell (f2, Q28)
@@ -89,8 +90,9 @@ __global__ void __launch_bounds__(256) k2_replay(const uint8_t *__restrict__ gim
   constexpr int GL = Seg<LPS, MM>::GL;
   extern __shared__ __align__(16) uint8_t smem[];
   __shared__ uint64_t mbar;
-  stage_image(smem, gimg, lay.bytes, &mbar);
-  const SmemProf P = smem_prof(smem, lay);
+  stage_image(smem, gimg, a.stage_bytes, &mbar);
+  SmemProf P = smem_prof(smem, lay);
+  if (a.stage_bytes < lay.bytes) P.hb = gimg;  // H tables stay in global memory (L1-cached)
   const Seg<LPS, MM> sg;
   const int g = sg.grp;
   const int M = P.M;
@@ -397,19 +399,20 @@ template <int LPS, int MM>
 cudaError_t launch_t(const uint8_t *img, const ImgLayout &lay, const ReplayArgs &a, cudaStream_t st, int sms) {
   // Algorithm 1 alone compiles without the policy code (no cost on the bench path)
   auto kern = lay.pol_mask == (1u << ES_POLICY_EDGESERVING) ? k2_replay<LPS, MM, false> : k2_replay<LPS, MM, true>;
-  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lay.bytes);
+  const size_t dyn = a.stage_bytes;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
   if (e != cudaSuccess) return e;
   // threads per block: the smallest of 64 / 128 / 256 that keeps the resident
   // thread count of 256-thread blocks (small blocks deal the longest-first
   // scenarios round-robin over the SMs in finer grains; a large profile image
   // -- one CTA per SM by shared memory -- keeps 256).  ES_K2_BLOCK overrides.
   int occ = 0;
-  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 256, lay.bytes);
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 256, dyn);
   if (e != cudaSuccess) return e;
   int threads = 256;
   for (int t = 64; t < 256; t *= 2) {
     int o = 0;
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, kern, t, lay.bytes);
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, kern, t, dyn);
     if (e != cudaSuccess) return e;
     if (o * t >= occ * 256) {
       threads = t;
@@ -421,7 +424,7 @@ cudaError_t launch_t(const uint8_t *img, const ImgLayout &lay, const ReplayArgs 
     const int v = atoi(env);
     if (v == 32 || v == 64 || v == 128 || v == 256) {
       threads = v;
-      e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, threads, lay.bytes);
+      e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, threads, dyn);
       if (e != cudaSuccess) return e;
     }
   }
@@ -432,7 +435,7 @@ cudaError_t launch_t(const uint8_t *img, const ImgLayout &lay, const ReplayArgs 
   const int64_t cap = (int64_t)sms * occ;
   if (blocks > cap) blocks = cap;
   if (blocks < 1) blocks = 1;
-  kern<<<(unsigned)blocks, threads, lay.bytes, st>>>(img, lay, a);
+  kern<<<(unsigned)blocks, threads, dyn, st>>>(img, lay, a);
   return cudaGetLastError();
 }
 
@@ -478,6 +481,9 @@ cudaError_t launch_replay(const uint8_t *img, const ImgLayout &lay, const es_tra
   a.dstat = dstat;
   a.work = reinterpret_cast<unsigned long long *>(work_ctr);
   a.order = nullptr;
+  // a large image (many SLOs: cfg3's nine, cfg4's sixteen) would leave one CTA
+  // per SM: stage only the core and read H (one load per candidate) from global
+  a.stage_bytes = lay.bytes > 64u * 1024u ? lay.core_bytes : lay.bytes;
   constexpr uint32_t SCORE_POLS =
       (1u << ES_POLICY_EDGESERVING) | (1u << ES_POLICY_ALLFINAL_DA) | (1u << ES_POLICY_OURS_BS1);
   constexpr uint32_t GRID_POLS = 1u << ES_POLICY_GRID;
