@@ -414,7 +414,9 @@ cudaError_t launch_t(const uint8_t *img, const ImgLayout &lay, const ReplayArgs 
     int o = 0;
     e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, kern, t, dyn);
     if (e != cudaSuccess) return e;
-    if (o * t >= occ * 256) {
+    // (and only while the extra per-CTA image copies leave L1 room: the
+    // pending waits are re-read from L1 every decision)
+    if (o * t >= occ * 256 && (size_t)o * dyn <= 72u * 1024u) {
       threads = t;
       occ = o;
       break;
