@@ -399,10 +399,17 @@ __device__ __forceinline__ Decision select_simple(const Seg<LPS, MM> &sg, const 
   return d;
 }
 
-#ifndef ES_WU
-#define ES_WU 2
+// positions per lane per step in the G loops: 2 when a segment is 8/16 lanes
+// (short queues: fewer predicated-off loads on the chain), 4 for whole-warp
+// segments (8 models; deep queues want more loads in flight); ES_WU overrides
+template <int LPS>
+__device__ __forceinline__ constexpr int wu_of() {
+#ifdef ES_WU
+  return ES_WU;
+#else
+  return LPS == 32 ? 4 : 2;
 #endif
-constexpr int WU = ES_WU;  // positions per lane per step in the G loops
+}
 
 // f2 GRID (Q28): every admissible (m, e, b) of every segment, in a
 // warp-uniform (m, e, b index) sweep with per-segment validity; per cell the
@@ -504,6 +511,7 @@ __device__ __forceinline__ Decision decide_general(const Seg<LPS, MM> &sg, const
       else U[m] += gw;
     }
   }
+  constexpr int WU = wu_of<LPS>();
   for (; p < len; p += WU * GL) {
     uint32_t w[WU];
 #pragma unroll
@@ -569,6 +577,7 @@ __device__ __forceinline__ Decision decide(const Seg<LPS, MM> &sg, const SmemPro
   // per-candidate clip tests and 3 M reductions collapse to 4 reductions.
   if (fast) {
     uint64_t tot = 0ull, srv = 0ull;
+    constexpr int WU = wu_of<LPS>();
     // WU positions per lane per step: their loads issue back to back (the
     // per-decision chain is latency-bound, one queue is a handful of steps)
     for (uint32_t p0 = sg.gl; p0 < len; p0 += WU * GL) {
