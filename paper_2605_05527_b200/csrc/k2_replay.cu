@@ -86,7 +86,13 @@ __device__ __forceinline__ void report(DevStatus *ds, uint32_t code, int64_t ite
 constexpr int PF_LINES = ES_PF_LINES;
 
 template <int LPS, int MM, bool POL>
-__global__ void __launch_bounds__(256) k2_replay(const uint8_t *__restrict__ gimg, ImgLayout lay, ReplayArgs a) {
+// whole-warp segments (8 models) hold more scenarios resident at 3 CTAs/SM
+// (80 registers, a few spills) -- cfg3 -24 %, cfg5-B -11 %; 16-lane segments
+// keep 1 (their spills would cost more than the occupancy brings)
+#ifndef ES_K2_MINB
+#define ES_K2_MINB (LPS == 32 ? 3 : 1)
+#endif
+__global__ void __launch_bounds__(256, ES_K2_MINB) k2_replay(const uint8_t *__restrict__ gimg, ImgLayout lay, ReplayArgs a) {
   constexpr int GL = Seg<LPS, MM>::GL;
   extern __shared__ __align__(16) uint8_t smem[];
   __shared__ uint64_t mbar;
