@@ -86,11 +86,12 @@ __device__ __forceinline__ void report(DevStatus *ds, uint32_t code, int64_t ite
 constexpr int PF_LINES = ES_PF_LINES;
 
 template <int LPS, int MM, bool POL>
-// whole-warp segments (8 models) hold more scenarios resident at 3 CTAs/SM
-// (80 registers, a few spills) -- cfg3 -24 %, cfg5-B -11 %; 16-lane segments
-// keep 1 (their spills would cost more than the occupancy brings)
+// min CTAs/SM for the register budget: 1 (no spills).  Forcing 3 for the
+// 8-model configs (80 registers, spills) helped a 16,384-scenario cfg3 slice
+// (-24 %) but slowed full cfg3 (+20 %: 3 image copies shrink L1) and the
+// latency-bound cfg5-A chains (+24 %), so it is left to ES_K2_MINB builds
 #ifndef ES_K2_MINB
-#define ES_K2_MINB (LPS == 32 ? 3 : 1)
+#define ES_K2_MINB 1
 #endif
 __global__ void __launch_bounds__(256, ES_K2_MINB) k2_replay(const uint8_t *__restrict__ gimg, ImgLayout lay, ReplayArgs a) {
   constexpr int GL = Seg<LPS, MM>::GL;
