@@ -86,14 +86,17 @@ __device__ __forceinline__ void report(DevStatus *ds, uint32_t code, int64_t ite
 constexpr int PF_LINES = ES_PF_LINES;
 
 template <int LPS, int MM, bool POL>
-// min CTAs/SM for the register budget: 1 (no spills).  Forcing 3 for the
-// 8-model configs (80 registers, spills) helped a 16,384-scenario cfg3 slice
-// (-24 %) but slowed full cfg3 (+20 %: 3 image copies shrink L1) and the
-// latency-bound cfg5-A chains (+24 %), so it is left to ES_K2_MINB builds
-#ifndef ES_K2_MINB
-#define ES_K2_MINB 1
+// register budget: ptxas's own (127 registers for 8-model segments: 2 CTAs
+// per SM; an explicit minimum of 1 CTA gives 136 and one CTA).  Forcing 3 CTAs
+// (80 registers, spills) helped a 16,384-scenario cfg3 slice (-24 %) but
+// slowed full cfg3 and the latency-bound cfg5-A chains, so it is left to
+// ES_K2_MINB builds
+#ifdef ES_K2_MINB
+#define ES_K2_BOUNDS __launch_bounds__(256, ES_K2_MINB)
+#else
+#define ES_K2_BOUNDS __launch_bounds__(256)
 #endif
-__global__ void __launch_bounds__(256, ES_K2_MINB) k2_replay(const uint8_t *__restrict__ gimg, ImgLayout lay, ReplayArgs a) {
+__global__ void ES_K2_BOUNDS k2_replay(const uint8_t *__restrict__ gimg, ImgLayout lay, ReplayArgs a) {
   constexpr int GL = Seg<LPS, MM>::GL;
   extern __shared__ __align__(16) uint8_t smem[];
   __shared__ uint64_t mbar;
