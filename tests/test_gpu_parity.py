@@ -574,3 +574,19 @@ def test_k1_stream_extreme_shapes(monkeypatch):
     o = es.es_score_candidates(h, to_dev(q_off, torch.uint64), to_dev(w, torch.uint32))
     torch.cuda.synchronize()
     assert_k1_equal({k: np_of(v) for k, v in o.items()}, oracle.decide_batch(prof, cfgs, q_off, w), M)
+
+
+def test_k2_launch_shape_invariance(monkeypatch):
+    """The scenario hand-out order (longest span first vs index order), the CTA
+    size and the image staging (full vs core-only with H from global) change
+    where and when scenarios run, never their results."""
+    w = inputs.workload("cfg3", scen_ids=list(range(0, 90, 4)), n_req=1200)  # nine SLOs: 145 KB image
+    ref = oracle.replay_batch(w.profile, w.cfgs, w.traces, dec_cap=2000, nthreads=8)
+    for env in [{}, {"ES_K2_ORDER": "0"}, {"ES_K2_BLOCK": "64"}, {"ES_K2_BLOCK": "256", "ES_K2_ORDER": "0"}]:
+        for k in ["ES_K2_ORDER", "ES_K2_BLOCK"]:
+            monkeypatch.delenv(k, raising=False)
+        for k, v in env.items():
+            monkeypatch.setenv(k, v)
+        g = run_k2(w, dec_cap=2000)
+        assert g["_code"] == 0
+        assert_k2_equal(g, ref, 2000)
