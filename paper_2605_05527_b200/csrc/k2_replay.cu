@@ -277,7 +277,7 @@ __global__ void ES_K2_BOUNDS k2_replay(const uint8_t *__restrict__ gimg, ImgLayo
           }
         }
       }
-      const uint32_t nq = __popc(sg.sbits(__ballot_sync(FULL, sg.gl == 0 && len > 0u)));
+      const uint32_t nq = __popc(sg.sbits(b_has)) / (uint32_t)GL;  // non-empty queues (all GL lanes of a group agree)
       const uint32_t ncand = grid ? ngrid : nq;  // scored candidates: queues, or (m, e, b) cells
       // a8: commit
       const int src = (int)(d.m & (MM - 1)) * GL;
