@@ -111,8 +111,10 @@ typedef struct {
  *                scored like Eq. 4 with L(m, e, b) and b served tasks; argmin of (S, m, e, b
  *                index) (the north star's "1,280 candidates per decision", f2; Q28)
  * A fixed exit is feasible iff w_head + L <= tau.  LQF / EDF policies score
- * nothing: the decision's S is 0.  Replay (es_replay_traces) accepts every
- * policy; es_score_candidates (K1) scores EdgeServing only (ES_ERR_ARG).
+ * nothing: the decision's S is 0 and their candidate scores are UINT64_MAX;
+ * under GRID a model's candidate score is its best cell.  Replay
+ * (es_replay_traces) accepts every policy; es_score_candidates (K1) every
+ * policy but SYMPHONY (ES_ERR_ARG: its "wait until" needs a replay clock).
  */
 #define ES_POLICY_EDGESERVING 0u
 #define ES_POLICY_ALL_FINAL 1u

@@ -307,9 +307,8 @@ es_status es_score_candidates(const es_profile *p, const es_snapshots *sn, es_de
   if (!sn->q_off || !sn->waits_us || !out->m || !out->e || !out->B || !out->L_us || !out->score_q || !out->flags)
     return fail(ES_ERR_ARG, "null snapshot input or decision output pointer");
   for (size_t k = 0; k < p->cfgs.size(); ++k)
-    if (p->cfgs[k].policy != ES_POLICY_EDGESERVING)
-      return fail(ES_ERR_ARG, "es_score_candidates scores EdgeServing only (cfg %zu has policy %u)", k,
-                  p->cfgs[k].policy);
+    if (p->cfgs[k].policy == ES_POLICY_SYMPHONY)
+      return fail(ES_ERR_ARG, "es_score_candidates: deferred batching (cfg %zu) needs a replay clock", k);
   DeviceGuard guard(p->device);
   CK(launch_score(p->d_img, p->lay, *sn, *out, p->d_status, (cudaStream_t)stream, p->sms), "k1_score");
   const_cast<es_profile *>(p)->launches++;

@@ -420,12 +420,13 @@ __device__ __forceinline__ constexpr int wu_of() {
 template <int LPS, int MM, class WaitAt>
 __device__ __noinline__ Decision decide_grid(const Seg<LPS, MM> &sg, const SmemProf &P, const SmemCfg &C,
                                              uint32_t len, uint32_t c, uint32_t wmax, WaitAt wait_at,
-                                             uint32_t &ncells) {
+                                             uint32_t &ncells, uint64_t &own_best) {
   constexpr int GL = Seg<LPS, MM>::GL;
   uint64_t bS = ~0ull;
   uint32_t bidx = 0xFFFFFFFFu, bm = 0xFFu, be = 0u, bB = 0u, bL = 0u;
   bool bfeas = false;
   ncells = 0u;
+  own_best = ~0ull;  // best cell of this lane's group model (the candidate score K1 reports)
   const uint32_t cpre = sg.sum(sg.gl == 0 ? c : 0u);
   const uint64_t *Hq = reinterpret_cast<const uint64_t *>(P.hb + C.off_H);
   for (int m = 0; m < P.M; ++m) {
@@ -459,6 +460,7 @@ __device__ __noinline__ Decision decide_grid(const Seg<LPS, MM> &sg, const SmemP
             S += (hi << (64 - F)) | (lo >> F);
           }
           ncells++;
+          if (sg.grp == m && S < own_best) own_best = S;
           if (S < bS || (S == bS && (uint32_t)cell < bidx)) {
             bS = S;
             bidx = (uint32_t)cell;

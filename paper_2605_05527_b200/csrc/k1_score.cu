@@ -32,7 +32,7 @@ struct ScoreArgs {
   DevStatus *dstat;
 };
 
-template <int LPS, int MM>
+template <int LPS, int MM, bool POL>
 __global__ void __launch_bounds__(256) k1_score(const uint8_t *__restrict__ gimg, ImgLayout lay, ScoreArgs a) {
   constexpr int GL = Seg<LPS, MM>::GL;
   constexpr int SPW = 32 / LPS;  // segments per warp
@@ -78,16 +78,39 @@ __global__ void __launch_bounds__(256) k1_score(const uint8_t *__restrict__ gimg
       }
     }
     const uint32_t c = srch ? phi : 0u;
-    const Cand cand = cand_params<LPS, MM>(sg, P, C, len, wmax);
+    const Cand cand = cand_params<LPS, MM, POL>(sg, P, C, len, wmax);
     bool bad = false;
     const bool fast = !__any_sync(FULL, len > 0u && wmax >= C.fast_lim);
-    const Decision d = decide<LPS, MM>(sg, P, C, len, c, fast, cand, [&](uint32_t p) {
+    auto wait_at = [&](uint32_t p) {
       const uint32_t w = __ldg(W + p);
       // read-window validation: head-first waits must not increase (Q7)
       if (p > c && w > __ldg(W + p - 1)) bad = true;
       if (w >= C.x_c) bad = true;
       return w;
-    });
+    };
+    // Eq. 7 on the stability score, or a baseline policy (Q26) / GRID (Q28):
+    // each branch runs warp-wide when some segment of the warp needs it
+    const bool sc = !POL || policy_scores(C.policy);
+    const bool grid = POL && C.policy == ES_POLICY_GRID;
+    Decision d{};
+    uint64_t own_grid = ~0ull;
+    if (!POL || __any_sync(FULL, sc)) d = decide<LPS, MM>(sg, P, C, len, c, fast, cand, wait_at);
+    if (POL && __any_sync(FULL, !sc && !grid)) {
+      const Decision ds = select_simple<LPS, MM>(sg, cand, len, wmax, C);
+      if (!sc && !grid) {
+        d = ds;
+        for (uint32_t p = c + sg.gl; p < len; p += GL) (void)wait_at(p);  // the read window's Q24 check
+      }
+    }
+    if (POL && __any_sync(FULL, grid)) {
+      uint32_t ng = 0u;
+      uint64_t own = ~0ull;
+      const Decision dg = decide_grid<LPS, MM>(sg, P, C, len, c, wmax, wait_at, ng, own);
+      if (grid) {
+        d = dg;
+        own_grid = own;
+      }
+    }
     const bool anybad = sg.seg_any(bad) || !cfg_ok;
     const bool nowork = !sg.seg_any(len > 0u);
     if (live_s && sg.sl == 0) {
@@ -104,13 +127,14 @@ __global__ void __launch_bounds__(256) k1_score(const uint8_t *__restrict__ gimg
         a.flags[s] = d.feas ? ES_FLAG_FEASIBLE : 0u;
       }
     }
-    if (live_s && a.cand && sg.gl == 0 && g < M) a.cand[s * M + g] = (anybad || len == 0u) ? ~0ull : d.S_own;
+    const uint64_t own_score = sc ? d.S_own : (grid ? own_grid : ~0ull);  // LQF / EDF policies score nothing
+    if (live_s && a.cand && sg.gl == 0 && g < M) a.cand[s * M + g] = (anybad || len == 0u) ? ~0ull : own_score;
   }
 }
 
 template <int LPS, int MM>
 cudaError_t launch_t(const uint8_t *img, const ImgLayout &lay, const ScoreArgs &a, cudaStream_t st, int sms) {
-  auto kern = k1_score<LPS, MM>;
+  auto kern = lay.pol_mask == (1u << ES_POLICY_EDGESERVING) ? k1_score<LPS, MM, false> : k1_score<LPS, MM, true>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lay.bytes);
   if (e != cudaSuccess) return e;
   int occ = 0;
@@ -423,8 +447,10 @@ cudaError_t launch_score(const uint8_t *img, const ImgLayout &lay, const es_snap
   // deep snapshots (>= 1024 waits each on average): one CTA per snapshot
   const char *k1 = getenv("ES_K1");
   const bool deep = sn.n_waits > 0 && sn.n > 0 && sn.n_waits / sn.n >= 1024;
-  if (k1 ? strcmp(k1, "stream") == 0 : deep) return launch_score_stream(img, lay, sn, out, dstat, st, sms);
-  if (k1 && strcmp(k1, "block") == 0) {
+  // the baseline policies and GRID run on the warp-segment mapping only
+  const bool pol = lay.pol_mask != (1u << ES_POLICY_EDGESERVING);
+  if (!pol && (k1 ? strcmp(k1, "stream") == 0 : deep)) return launch_score_stream(img, lay, sn, out, dstat, st, sms);
+  if (!pol && k1 && strcmp(k1, "block") == 0) {
     if (lay.M <= 2) return launch_block<2>(img, lay, a, st, sms);
     if (lay.M <= 4) return launch_block<4>(img, lay, a, st, sms);
     return launch_block<8>(img, lay, a, st, sms);

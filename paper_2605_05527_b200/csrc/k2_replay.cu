@@ -254,8 +254,9 @@ __global__ void ES_K2_BOUNDS k2_replay(const uint8_t *__restrict__ gimg, ImgLayo
       uint32_t ngrid = 0u;
       if (POL && a.any_grid && __any_sync(FULL, dec && grid)) {
         uint32_t ng = 0u;
+        uint64_t own = 0ull;
         const Decision dg = decide_grid<LPS, MM>(sg, P, C, len, c, wmax, [&](uint32_t p) { return tt - ldg_u32(Ah + p); },
-                                                 ng);
+                                                 ng, own);
         if (grid) {
           d = dg;
           ngrid = ng;

@@ -521,13 +521,36 @@ def test_k2_mixed_policies_in_one_warp():
     assert_k2_equal(g, o, cap)
 
 
-def test_k1_rejects_baseline_policies():
-    """es_score_candidates scores EdgeServing only (include/edgeserve.h)."""
+def test_k1_rejects_deferred_batching():
+    """es_score_candidates scores every policy but SYMPHONY (its wait-until
+    needs a replay clock; include/edgeserve.h)."""
     prof = inputs.synth_profile(2, 2, [1, 2])
-    h = es.es_load_profile(prof, [inputs.SchedCfg(tau=50000, b_max=2, policy=3)])
+    h = es.es_load_profile(prof, [inputs.SchedCfg(tau=50000, b_max=2, policy=7)])
     q_off, w = inputs.snapshots_uniform(1, 4, 2, 3, 100000)
     with pytest.raises(es.EsError):
         es.es_score_candidates(h, to_dev(q_off, torch.uint64), to_dev(w, torch.uint32))
+
+
+@pytest.mark.parametrize("M", [3, 8])
+def test_k1_policies(M):
+    """K1 under the baseline / ablation policies and GRID (Q26, Q28), one cfg
+    per policy interleaved snapshot by snapshot: decisions, scores (per-model
+    best cell under GRID, none under LQF / EDF) and flags equal the oracle,
+    with inversions planted in some snapshots (flagged bad, Q24)."""
+    pols = [p for p in POLICY_IDS if p != "symphony"]
+    prof = inputs.synth_profile(M, 4, [1, 2, 4, 8], L_top=20000.0)
+    cfgs = [inputs.SchedCfg(tau=50000, b_max=6, policy=POLICY_IDS[p]) for p in pols]
+    n = 1800
+    q_off, w = inputs.snapshots_uniform(60 + M, n, M, 9, 150000)
+    w = w.copy()
+    rng = np.random.default_rng(M)
+    for s in rng.choice(n, 40, replace=False):
+        m = int(rng.integers(M))
+        lo, hi = int(q_off[s * M + m]), int(q_off[s * M + m + 1])
+        if hi - lo >= 2:
+            w[hi - 1] = w[hi - 2] + 1
+    ci = (np.arange(n) % len(pols)).astype(np.uint16)
+    assert_k1_equal(run_k1(prof, cfgs, q_off, w, ci), oracle.decide_batch(prof, cfgs, q_off, w, ci), M)
 
 
 @pytest.mark.parametrize("fast", ["tma", "regs"])
