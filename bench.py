@@ -376,6 +376,27 @@ def main():
             "hbm_view": {"alg_bytes_per_launch": alg_bytes, "achieved_gbs": alg_bytes / k2_avg_s / 1e9,
                          "peak_gbs": hbm, "frac": alg_bytes / k2_avg_s / 1e9 / hbm}}
 
+    # chain view: K2 is bound by its longest dependent chain of decisions; the
+    # longest scenario replayed alone on the GPU is that chain's latency floor
+    if not args.ncu:
+        s_max = int(np.argmax(st[:, 0]))
+        w1 = inputs.workload(args.workload, scen_ids=np.array([rank * S + s_max], np.int64))
+        d1 = engine.upload_traces(w1.traces, dev)
+        o1 = es.alloc_replay_out(h, 1, int(w1.traces.arrival.size), dev, full=False, p95=False)
+        t1 = []
+        for i in range(4):
+            a1, b1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a1.record(stream)
+            es.es_replay_traces(h, d1["arr_off"], d1["arrival"], d1["cfg_idx"], d1["group_id"], out=o1, full=False,
+                                p95=False, stream=stream)
+            b1.record(stream)
+            torch.cuda.synchronize()
+            if i:
+                t1.append(a1.elapsed_time(b1))
+        alone = statistics.median(t1)
+        roof["chain_view"] = {"longest_chain_decisions": int(st[s_max, 0]), "alone_ms": alone,
+                              "k2_ms": statistics.mean(k2_ms), "frac": alone / statistics.mean(k2_ms),
+                              "note": "longest scenario replayed alone = the batch's latency floor; frac = floor / K2"}
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "u32", "data": "synthetic",
