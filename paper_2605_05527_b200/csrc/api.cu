@@ -10,6 +10,7 @@
 
 #include <cmath>
 #include <algorithm>
+#include <atomic>
 #include <cstdarg>
 #include <cstdio>
 #include <cstdlib>
@@ -27,10 +28,9 @@ struct es_profile {
   ImgLayout lay{};
   uint8_t *d_img = nullptr;
   DevStatus *d_status = nullptr;
-  uint32_t *d_work = nullptr;  // 8 bytes: scenario work counter of K2
   std::vector<es_sched_cfg> cfgs;
   std::vector<uint8_t> h_img;  // host copy (after table build)
-  int64_t launches = 0;
+  std::atomic<int64_t> launches{0};  // kernel launches (calls may come from several host threads)
   // scratch for es_replay_traces_host (double-buffered by the pipelined call)
   uint8_t *scratch = nullptr;
   size_t scratch_bytes = 0;
@@ -239,7 +239,6 @@ es_status es_load_profile(const es_profile_desc *desc, const es_sched_cfg *cfgs,
   cudaError_t e;
   if ((e = cudaMalloc(&p->d_img, lay.bytes)) != cudaSuccess) return cleanup(cuda_fail(e, "cudaMalloc(image)"));
   if ((e = cudaMalloc(&p->d_status, sizeof(DevStatus))) != cudaSuccess) return cleanup(cuda_fail(e, "cudaMalloc(status)"));
-  if ((e = cudaMalloc(&p->d_work, 16)) != cudaSuccess) return cleanup(cuda_fail(e, "cudaMalloc(work)"));
   if ((e = cudaMemset(p->d_status, 0, sizeof(DevStatus))) != cudaSuccess) return cleanup(cuda_fail(e, "memset"));
   if ((e = cudaMemcpy(p->d_img, img.data(), lay.bytes, cudaMemcpyHostToDevice)) != cudaSuccess)
     return cleanup(cuda_fail(e, "upload image"));
@@ -266,7 +265,6 @@ es_status es_free_profile(es_profile *p) {
   DeviceGuard guard(p->device);
   cudaFree(p->d_img);
   cudaFree(p->d_status);
-  cudaFree(p->d_work);
   cudaFree(p->scratch);
   cudaFree(p->scratch2);
   if (p->copy_stream) {
@@ -324,21 +322,9 @@ es_status es_replay_traces(const es_profile *p, const es_traces *tr, es_replay_o
   if (out->dec_cap < 0) return fail(ES_ERR_ARG, "dec_cap < 0");
   DeviceGuard guard(p->device);
   es_profile *pm = const_cast<es_profile *>(p);
-  // K2 mapping: lane segments per scenario (k2_replay.cu, default) or
-  // ES_K2=lane: one lane per model queue (k2_lane.cu; same integers)
-  const char *k2 = getenv("ES_K2");
-  bool any_policy = false;  // the lane mapping replays EdgeServing only
-  for (const es_sched_cfg &c : p->cfgs) any_policy |= c.policy != ES_POLICY_EDGESERVING;
-  if (!(k2 && strcmp(k2, "lane") == 0) || any_policy) {
-    int nl = 0;
-    CK(launch_replay(p->d_img, p->lay, *tr, *out, p->d_status, p->d_work, (cudaStream_t)stream, p->sms, &nl),
-       "k2_replay");
-    pm->launches += nl;
-  } else {
-    CK(launch_replay_lane(p->d_img, p->lay, *tr, *out, p->d_status, p->d_work, (cudaStream_t)stream, p->sms),
-       "k2_lane");
-    pm->launches++;
-  }
+  int nl = 0;
+  CK(launch_replay(p->d_img, p->lay, *tr, *out, p->d_status, (cudaStream_t)stream, p->sms, &nl), "k2_replay");
+  pm->launches += nl;
   if (out->scen_p95_us) {
     CK(launch_scen_p95(p->d_img, p->lay, *tr, *out, (cudaStream_t)stream, p->sms), "k3_scen_p95");
     pm->launches++;
@@ -614,6 +600,6 @@ es_status es_device_status(es_profile *p, es_stream stream, uint32_t *code, int6
   return ES_OK;
 }
 
-int64_t es_launch_count(const es_profile *p) { return p ? p->launches : 0; }
+int64_t es_launch_count(const es_profile *p) { return p ? p->launches.load() : 0; }
 
 }  // extern "C"

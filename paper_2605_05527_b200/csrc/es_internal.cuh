@@ -60,11 +60,7 @@ cudaError_t launch_score(const uint8_t *img, const ImgLayout &lay, const es_snap
 cudaError_t launch_score_stream(const uint8_t *img, const ImgLayout &lay, const es_snapshots &sn,
                                 const es_decisions &out, DevStatus *dstat, cudaStream_t st, int sms);
 cudaError_t launch_replay(const uint8_t *img, const ImgLayout &lay, const es_traces &tr,
-                          const es_replay_out &out, DevStatus *dstat, uint32_t *work_ctr,
-                          cudaStream_t st, int sms, int *n_launch);
-cudaError_t launch_replay_lane(const uint8_t *img, const ImgLayout &lay, const es_traces &tr,
-                               const es_replay_out &out, DevStatus *dstat, uint32_t *work_ctr, cudaStream_t st,
-                               int sms);
+                          const es_replay_out &out, DevStatus *dstat, cudaStream_t st, int sms, int *n_launch);
 cudaError_t launch_scen_p95(const uint8_t *img, const ImgLayout &lay, const es_traces &tr,
                             const es_replay_out &out, cudaStream_t st, int sms);
 cudaError_t launch_stats_fused(const uint8_t *img, const ImgLayout &lay, const es_traces &tr,

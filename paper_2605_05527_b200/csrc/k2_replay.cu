@@ -28,36 +28,12 @@
 
 #include <algorithm>
 #include <cstdlib>
+#include <cstring>
 
-#include "decide.cuh"
+#include "k2_common.cuh"
 
 namespace es {
 namespace {
-
-struct ReplayArgs {
-  int64_t n_scen;
-  const uint16_t *cfg_idx;
-  const uint64_t *arr_off;
-  const uint32_t *arrival;
-  uint32_t *completion;
-  uint8_t *exit_used;
-  uint32_t *lat;
-  uint64_t *stats;
-  int64_t dec_cap;
-  uint32_t *dec_t;
-  uint8_t *dec_m, *dec_e;
-  uint16_t *dec_B;
-  uint32_t *dec_L;
-  uint64_t *dec_S;
-  uint8_t *dec_f;
-  DevStatus *dstat;
-  unsigned long long *work;
-  const uint32_t *order;  // scenario hand-out order (longest traces first), or null
-  uint32_t stage_bytes;   // image bytes staged in shared memory (core only: H read from global)
-  bool any_simple;  // some cfg selects by LQF / EDF / deferred batching (Q26, Q27)
-  bool any_score;   // some cfg selects by the stability score (Eq. 7)
-  bool any_grid;    // some cfg scores every (m, e, b) cell (f2, Q28)
-};
 
 __device__ __forceinline__ uint32_t ldg_u32(const uint32_t *p) { return __ldg(p); }
 
@@ -76,16 +52,15 @@ __device__ __forceinline__ bool segs_idle(unsigned b_go, unsigned b_has) {
   return idle;
 }
 
-__device__ __forceinline__ void report(DevStatus *ds, uint32_t code, int64_t item) {
-  if (atomicCAS(&ds->code, 0u, code) == 0u) ds->item = (unsigned long long)item;
-}
 
 #ifndef ES_PF_LINES
 #define ES_PF_LINES 2
 #endif
 constexpr int PF_LINES = ES_PF_LINES;
 
-template <int LPS, int MM, bool POL>
+template <int LPS, int MM, bool POL, bool OUT>
+// OUT = false compiles the stats-only replay (no completion / exit / decision
+// log outputs: the bench and sweep path) without their per-decision tests.
 // register budget: ptxas's own (127 registers for 8-model segments: 2 CTAs
 // per SM; an explicit minimum of 1 CTA gives 136 and one CTA).  Forcing 3 CTAs
 // (80 registers, spills) helped a 16,384-scenario cfg3 slice (-24 %) but
@@ -311,7 +286,7 @@ __global__ void ES_K2_BOUNDS k2_replay(const uint8_t *__restrict__ gimg, ImgLayo
               viol += T > C.tau ? 1u : 0u;  // Eq. 2, strict
             }
           }
-          if (a.dec_cap && sg.sl == 0 && (int64_t)decisions <= a.dec_cap) {
+          if (OUT && a.dec_cap && sg.sl == 0 && (int64_t)decisions <= a.dec_cap) {
             const int64_t o = s * a.dec_cap + (int64_t)decisions - 1;
             if (a.dec_t) a.dec_t[o] = t;
             if (a.dec_m) a.dec_m[o] = (uint8_t)d.m;
@@ -409,7 +384,10 @@ __global__ void k2_order_scatter(int64_t n_scen, const uint32_t *span, unsigned 
 template <int LPS, int MM>
 cudaError_t launch_t(const uint8_t *img, const ImgLayout &lay, const ReplayArgs &a, cudaStream_t st, int sms) {
   // Algorithm 1 alone compiles without the policy code (no cost on the bench path)
-  auto kern = lay.pol_mask == (1u << ES_POLICY_EDGESERVING) ? k2_replay<LPS, MM, false> : k2_replay<LPS, MM, true>;
+  const bool alg1 = lay.pol_mask == (1u << ES_POLICY_EDGESERVING);
+  const bool out = a.completion || a.exit_used || a.dec_cap;
+  auto kern = alg1 ? (out ? k2_replay<LPS, MM, false, true> : k2_replay<LPS, MM, false, false>)
+                   : (out ? k2_replay<LPS, MM, true, true> : k2_replay<LPS, MM, true, false>);
   const size_t dyn = a.stage_bytes;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
   if (e != cudaSuccess) return e;
@@ -459,21 +437,28 @@ cudaError_t launch_lps(const uint8_t *img, const ImgLayout &lay, const ReplayArg
   return launch_t<LPS, 8>(img, lay, a, st, sms);
 }
 
-// lanes per scenario: ES_LPS overrides; default 16 for M <= 4, 32 above
-int choose_lps(const ImgLayout &lay) {
+// lanes per scenario: a latency-bound batch (few chains per SM: the longest
+// chain is the kernel's time) takes wide segments -- 16 lanes for M <= 4, a
+// whole warp for M > 4 -- so one decision has more lanes on its chain; a
+// throughput-bound batch (>= 256 scenarios per SM) takes half that width, so
+// each warp instruction serves twice the decisions.  Measured (1 x B200, K2
+// alone): cfg2 16 lanes 2.90 ms vs 8 lanes 3.77; cfg5-A 32: 105 vs 16: 175;
+// cfg5-B 32: 281 vs 16: 323; cfg3 16: 46.7 vs 32: 55.0; cfg4 8: 52.5 vs
+// 16: 64.9.  ES_LPS overrides.
+int choose_lps(const ImgLayout &lay, int64_t n_scen, int sms) {
   const char *env = getenv("ES_LPS");
   if (env) {
     int v = atoi(env);
     if (v == 8 || v == 16 || v == 32) return v;
   }
-  return lay.M <= 4 ? 16 : 32;
+  const int wide = lay.M <= 4 ? 16 : 32;
+  return n_scen >= (int64_t)256 * sms ? wide / 2 : wide;
 }
 
 }  // namespace
 
 cudaError_t launch_replay(const uint8_t *img, const ImgLayout &lay, const es_traces &tr,
-                          const es_replay_out &out, DevStatus *dstat, uint32_t *work_ctr,
-                          cudaStream_t st, int sms, int *n_launch) {
+                          const es_replay_out &out, DevStatus *dstat, cudaStream_t st, int sms, int *n_launch) {
   ReplayArgs a;
   a.n_scen = tr.n_scen;
   a.cfg_idx = tr.cfg_idx;
@@ -492,7 +477,6 @@ cudaError_t launch_replay(const uint8_t *img, const ImgLayout &lay, const es_tra
   a.dec_S = out.dec_score_q;
   a.dec_f = out.dec_flags;
   a.dstat = dstat;
-  a.work = reinterpret_cast<unsigned long long *>(work_ctr);
   a.order = nullptr;
   // a large image (many SLOs: cfg3's nine, cfg4's sixteen) would leave one CTA
   // per SM: stage only the core and read H (one load per candidate) from global
@@ -503,17 +487,19 @@ cudaError_t launch_replay(const uint8_t *img, const ImgLayout &lay, const es_tra
   a.any_score = (lay.pol_mask & SCORE_POLS) != 0u;
   a.any_grid = (lay.pol_mask & GRID_POLS) != 0u;
   a.any_simple = (lay.pol_mask & ~(SCORE_POLS | GRID_POLS)) != 0u;
-  cudaError_t e = cudaMemsetAsync(work_ctr, 0, sizeof(unsigned long long), st);
-  if (e != cudaSuccess) return e;
-  *n_launch += 1;
-  // longest-span-first hand-out order (ES_K2_ORDER=0: scenario index order)
-  void *ord = nullptr;
+  // per-call scratch (stream-ordered, so concurrent calls on one handle never
+  // share it): the scenario work counter, and the longest-span-first hand-out
+  // order (ES_K2_ORDER=0: scenario index order)
   const char *oe = getenv("ES_K2_ORDER");
-  if (tr.n_scen > 1 && tr.n_scen < (int64_t)0xFFFFFFFF && !(oe && oe[0] == '0')) {
-    const size_t ob = 4u * (size_t)tr.n_scen, sb = 4u * (1 + 2 * NBK);
-    e = cudaMallocAsync(&ord, 2 * ob + sb, st);
-    if (e != cudaSuccess) return e;
-    uint32_t *order = static_cast<uint32_t *>(ord), *span = order + tr.n_scen;
+  const bool ordered = tr.n_scen > 1 && tr.n_scen < (int64_t)0xFFFFFFFF && !(oe && oe[0] == '0');
+  const size_t ob = ordered ? 4u * (size_t)tr.n_scen : 0u, sb = ordered ? 4u * (1 + 2 * NBK) : 0u;
+  void *buf = nullptr;
+  cudaError_t e = cudaMallocAsync(&buf, 16 + 2 * ob + sb, st);
+  if (e != cudaSuccess) return e;
+  a.work = static_cast<unsigned long long *>(buf);
+  e = cudaMemsetAsync(buf, 0, 16, st);
+  if (e == cudaSuccess && ordered) {
+    uint32_t *order = reinterpret_cast<uint32_t *>(static_cast<uint8_t *>(buf) + 16), *span = order + tr.n_scen;
     unsigned *sc = reinterpret_cast<unsigned *>(span + tr.n_scen);
     e = cudaMemsetAsync(sc, 0, sb, st);
     const int blocks = (int)std::min<int64_t>((tr.n_scen + 255) / 256, (int64_t)sms * 8);
@@ -521,19 +507,18 @@ cudaError_t launch_replay(const uint8_t *img, const ImgLayout &lay, const es_tra
     if (e == cudaSuccess) k2_order_hist<<<blocks, 256, 0, st>>>(tr.n_scen, span, sc);
     if (e == cudaSuccess) k2_order_scatter<<<blocks, 256, 0, st>>>(tr.n_scen, span, sc, order);
     if (e == cudaSuccess) e = cudaGetLastError();
-    if (e != cudaSuccess) return e;
     a.order = order;
     *n_launch += 3;
   }
-  const int lps = choose_lps(lay);
-  e = lps == 8 && lay.M <= 8 ? launch_lps<8>(img, lay, a, st, sms)
-      : lps == 16            ? launch_lps<16>(img, lay, a, st, sms)
-                             : launch_lps<32>(img, lay, a, st, sms);
-  if (ord) {
-    const cudaError_t f = cudaFreeAsync(ord, st);
-    if (e == cudaSuccess) e = f;
+  if (e == cudaSuccess) {
+    const int lps = choose_lps(lay, tr.n_scen, sms);
+    e = lps == 8 && lay.M <= 8 ? launch_lps<8>(img, lay, a, st, sms)
+        : lps == 16            ? launch_lps<16>(img, lay, a, st, sms)
+                               : launch_lps<32>(img, lay, a, st, sms);
+    *n_launch += 1;
   }
-  return e;
+  const cudaError_t f = cudaFreeAsync(buf, st);
+  return e != cudaSuccess ? e : f;
 }
 
 }  // namespace es

@@ -28,9 +28,12 @@ constexpr int NT = 256;
 constexpr int NW = NT / 32;
 constexpr int BINS = ES_HIST_BINS;  // 4096
 constexpr uint32_t COARSE_OVF = 4095u;
-// group state word 1: residual rank (low 32 bits) | mode << 32 | done << 40
-constexpr uint64_t MODE_OVF = 1ull << 32;
-constexpr uint64_t DONE = 1ull << 40;
+// group state [g][2]: word 0 = selected digit prefix (low 32 bits) | MODE_OVF
+// while the selection runs, the P95 itself once done; word 1 = the residual
+// rank as a full u64 (a group may hold far more than 2^32 completions), or
+// DONE.  Ranks are < 2^63, so neither flag bit can be taken by a value.
+constexpr uint64_t MODE_OVF = 1ull << 63;  // word 0: the rank lies among T >= 16.77 s
+constexpr uint64_t DONE = 1ull << 63;      // word 1: resolved (word 0 is the P95)
 
 // block-wide: find the bin holding rank k (1-based) in hist[0..nbins);
 // returns bin and writes the count strictly before it into *before.
@@ -129,7 +132,7 @@ __global__ void __launch_bounds__(NT) k3_stats(StatsArgs a) {
       continue;
     }
     const uint32_t *gsrc = a.lat + base + W;
-    const bool staged = n <= a.cap;
+    const bool staged = n + 3u <= a.cap;  // + up to 3 leading words of 16-byte alignment
     // stage the scenario's latencies into shared memory with TMA: one bulk copy
     // of the 16-byte aligned span [gsrc - off, ...) (off <= 3 leading words
     // ignored), the <= 3 trailing words loaded directly
@@ -259,10 +262,11 @@ __global__ void __launch_bounds__(NT) k_group_level(GroupArgs a) {
     const uint32_t g = a.group_id ? a.group_id[s] : 0u;
     if (g >= a.n_groups) continue;
     const uint64_t w1 = a.state[2 * g + 1];
-    if ((w1 & DONE) || (uint32_t)w1 == 0u) continue;  // resolved or empty group
-    const bool ovf = (w1 & MODE_OVF) != 0ull;
+    if ((w1 & DONE) || w1 == 0ull) continue;  // resolved or empty group
+    const uint64_t w0 = a.state[2 * g];
+    const bool ovf = (w0 & MODE_OVF) != 0ull;
     if (!ovf && a.level != 1) continue;
-    const uint32_t prefix = (uint32_t)a.state[2 * g];
+    const uint32_t prefix = (uint32_t)w0;
     const int k = a.cfg_idx ? (int)a.cfg_idx[s] : 0;
     const uint32_t W = a.cfg[k].warmup;
     const uint64_t base = a.arr_off[s * a.M];
@@ -321,35 +325,35 @@ __global__ void __launch_bounds__(NT) k_group_select(uint32_t n_groups, int leve
   } else {
     w0 = state[2 * g];
     w1 = state[2 * g + 1];
-    if ((w1 & DONE) || (uint32_t)w1 == 0u) return;
-    if (!(w1 & MODE_OVF) && level != 1) return;
+    if ((w1 & DONE) || w1 == 0ull) return;
+    if (!(w0 & MODE_OVF) && level != 1) return;
   }
-  const bool ovf = (w1 & MODE_OVF) != 0ull;
-  const uint64_t rank = (uint32_t)w1;
+  const bool ovf = (w0 & MODE_OVF) != 0ull;
+  w0 &= ~MODE_OVF;        // the digit prefix selected so far
+  const uint64_t rank = w1;  // full u64 residual rank
   const int nbins = (level == 3) ? 256 : BINS;
   uint64_t before;
   const uint32_t b = find_bin(hist + (uint64_t)g * BINS, nbins, rank, &before);
   if (threadIdx.x == 0) {
     const uint64_t r = rank - before;
-    uint64_t v, flags;
+    uint64_t v;
+    bool done = false, ovf_next = ovf;
     if (level == 0) {
       v = b;
-      flags = b == COARSE_OVF ? MODE_OVF : 0ull;
+      ovf_next = b == COARSE_OVF;
     } else if (!ovf) {  // level 1 normal: exact value
       v = ((uint64_t)w0 << 12) | b;
-      flags = DONE;
+      done = true;
     } else if (level == 1) {
       v = b;  // T >> 20
-      flags = MODE_OVF;
     } else if (level == 2) {
       v = ((uint64_t)w0 << 12) | b;  // T >> 8
-      flags = MODE_OVF;
     } else {
       v = ((uint64_t)w0 << 8) | b;  // T
-      flags = DONE;
+      done = true;
     }
-    state[2 * g] = v;
-    state[2 * g + 1] = (flags & DONE) ? DONE : (r | flags);
+    state[2 * g] = done ? v : (v | (ovf_next ? MODE_OVF : 0ull));
+    state[2 * g + 1] = done ? DONE : r;
   }
 }
 

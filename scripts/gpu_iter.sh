@@ -1,6 +1,10 @@
-# quick iteration: parity (gpu tests), bench K2 timing per LPS, ncu of K2 at the default LPS
-timeout 400 python -m pytest tests -m gpu -q --timeout 120 -x 2>&1 | tail -3 | tee gpurun_out/tests.log
-for L in ${LPS_LIST:-8 16}; do ES_LPS=$L timeout 150 python bench.py --steps 20 --warmup 3 --no-cpu-baseline --no-e2e 2>/dev/null | tail -1 | python -c "import json,sys; d=json.loads(sys.stdin.read()); print('LPS',$L, 'Gdec/s %.3f'%(d['value']/1e9), 'ms/step %.3f'%d['ms_per_step'], 'k2 ms %.3f'%d['roofline']['k2_ms'])"; done
-if [ -n "$NCU" ]; then
-  timeout 600 ncu --set full --clock-control none --import-source on -k regex:k2_replay -s 1 -c 1 -o gpurun_out/prof_k2_$NCU python bench.py --steps 1 --warmup 1 --ncu > gpurun_out/ncu_$NCU.log 2>&1; tail -1 gpurun_out/ncu_$NCU.log
-fi
+# quick GPU iteration: selected tests + a short cfg3 bench line (K2 only, no extras)
+T=${T:-"tests/test_gpu_parity.py -k both_mappings"}
+timeout 900 python -m pytest $T -x -q --timeout 600 2>&1 | tail -15 > gpurun_out/iter_tests.log
+for W in ${WL:-cfg3}; do
+  timeout 600 python bench.py --workload $W --steps 3 --warmup 3 --no-k1 --no-e2e --no-cpu-baseline > gpurun_out/iter_bench_$W.json 2> gpurun_out/iter_bench_$W.err
+done
+cat gpurun_out/iter_tests.log
+for W in ${WL:-cfg3}; do tail -2 gpurun_out/iter_bench_$W.err; python -c "
+import json,sys; d=json.load(open('gpurun_out/iter_bench_$W.json')); r=d['roofline']
+print('$W', 'value %.3e'%d['value'], 'ms/step %.2f'%d['ms_per_step'], 'k2_ms', r.get('k2_ms'), 'frac', r.get('frac'))"; done

@@ -415,16 +415,22 @@ def test_group_merge_overflow_bin():
     assert np.array_equal(g["p95"], o["p95"])
 
 
-def test_k2_lane_mapping_matches_oracle(monkeypatch):
-    """The alternative one-lane-per-model K2 mapping (ES_K2=lane) gives the
-    same bits as the oracle on cfg2/cfg3 subsets and the edge cases."""
-    monkeypatch.setenv("ES_K2", "lane")
-    for name, ids, n_req in [("cfg2", list(range(0, 60, 3)), 1500), ("cfg3", list(range(0, 54, 3)), 1200)]:
+@pytest.mark.parametrize("lps", ["8", "16", "32"])
+def test_k2_segment_widths(monkeypatch, lps):
+    """Every K2 segment width (ES_LPS = 8, 16, 32 lanes per scenario) gives the
+    oracle's bits on config subsets, deep overload (the general clip path),
+    the edge cases and the errors."""
+    monkeypatch.setenv("ES_LPS", lps)
+    for name, ids, n_req in [("cfg1", [0], None), ("cfg2", list(range(0, 60, 3)), 1500),
+                             ("cfg3", list(range(0, 117, 2)), 1500)]:
         w = inputs.workload(name, scen_ids=ids, n_req=n_req)
         g = run_k2(w, dec_cap=2000)
         o = oracle.replay_batch(w.profile, w.cfgs, w.traces, dec_cap=2000, nthreads=8)
+        assert g["_code"] == 0
         assert_k2_equal(g, o, 2000)
+    test_k2_deep_overload()
     test_k2_edge_cases()
+    test_k2_errors()
 
 
 @pytest.mark.parametrize("mode", ["stream", "block", "seg"])
