@@ -619,3 +619,161 @@ def test_k2_launch_shape_invariance(monkeypatch):
         g = run_k2(w, dec_cap=2000)
         assert g["_code"] == 0
         assert_k2_equal(g, ref, 2000)
+
+
+# ------------------------------------------------------------------ round-2 parity gaps
+
+@pytest.mark.parametrize("name", ["cfg2", "cfg3"])
+@pytest.mark.parametrize("exits", ["layer1+final", "layer3+final"])
+def test_k2_restricted_exit_masks(name, exits):
+    """K2 replay under the exit configurations of the paper's exit-point study
+    (the f3 sweep): only {layer1, final} or {layer3, final} allowed
+    for every model.  Eq. 6 searches the allowed exits only, the Q2 fallback is
+    the shallowest *allowed* exit, cells count allowed exits; compared element
+    by element (completions, exits, latencies, decision logs, counters)."""
+    w = inputs.workload(name, scen_ids=list(range(0, 117, 4)), n_req=1500)
+    E = w.profile.E
+    keep = [0, E - 1] if exits == "layer1+final" else [2, E - 1]
+    mask = np.zeros((w.profile.M, E), np.uint8)
+    mask[:, keep] = 1
+    prof = inputs.Profile(w.profile.M, E, w.profile.bs, w.profile.lat, mask)
+    w = inputs.Workload(w.name, prof, w.cfgs, w.traces, w.n_req)
+    g = run_k2(w, dec_cap=1500)
+    o = oracle.replay_batch(prof, w.cfgs, w.traces, dec_cap=1500, nthreads=8)
+    assert g["_code"] == 0
+    nd = np.minimum(o["stats"][:, 0], 1500).astype(np.int64)
+    valid = np.arange(1500)[None, :] < nd[:, None]
+    assert set(np.unique(o["dec_e"].reshape(-1, 1500)[valid])) <= set(keep)
+    assert_k2_equal(g, o, 1500)
+    # cells examined = decisions' non-empty queues x 2 allowed exits
+    assert np.array_equal(g["stats"][:, 2], 2 * g["stats"][:, 1])
+
+
+@pytest.mark.parametrize("mode", ["seg", "stream", "block"])
+def test_k1_q24_clipped_prefix_contract(monkeypatch, mode):
+    """Reading Q24 exactly: K1 counts the clipped prefix (waits >= x_c) by
+    search and never reads it, so an inversion planted *inside* that prefix is
+    not flagged: the kernel returns the decision of the same snapshot with the
+    prefix sorted, without ES_FLAG_BAD_INPUT, while the oracle (which checks
+    whole queues) flags it.  Its neighbours in the batch are unaffected."""
+    monkeypatch.setenv("ES_K1", mode)
+    M = 4
+    prof = inputs.synth_profile(M, 4, list(range(1, 17)))
+    cfgs = [inputs.SchedCfg(tau=50000, b_max=16)]
+    x_c = oracle.build_tables(50000, 10)["x_c"]
+    depth = 1500 if mode != "seg" else 24
+    q_off, w = inputs.snapshots_poisson_depth(3, np.arange(64), M, depth, [depth / 100000.0] * M)
+    w = w.copy()
+    lens = np.diff(q_off.astype(np.int64)).reshape(64, M)
+    targets = [s for s in range(3, 64, 7) if lens[s, s % M] >= 6][:3]
+    assert len(targets) == 3
+    fixed = w.copy()
+    for s in targets:
+        m = s % M
+        lo, hi = int(q_off[s * M + m]), int(q_off[s * M + m + 1])
+        # a clipped prefix of 4 tasks (w >= x_c) with an inversion between its
+        # 2nd and 3rd task; the rest of the queue stays below x_c
+        pre = np.array([x_c + 5000, x_c + 3000, x_c + 9000, x_c + 100], np.uint32)
+        w[lo:lo + 4] = pre
+        fixed[lo:lo + 4] = np.sort(pre)[::-1]
+        w[lo + 4:hi] = np.minimum(w[lo + 4:hi], x_c - 1)
+        fixed[lo + 4:hi] = w[lo + 4:hi]
+    g = run_k1(prof, cfgs, q_off, w)
+    ref_bad = oracle.decide_batch(prof, cfgs, q_off, w)
+    ref_fix = oracle.decide_batch(prof, cfgs, q_off, fixed)
+    assert (ref_bad["flags"][targets] & 4).all()  # the oracle checks whole queues
+    assert not (g["flags"][targets] & 4).any()  # the kernel does not read the prefix
+    for k in ["m", "e", "B", "L", "S", "flags"]:
+        assert np.array_equal(g[k], ref_fix[k]), k  # = the decision with the prefix sorted, every snapshot
+    others = np.setdiff1d(np.arange(64), targets)
+    assert np.array_equal(g["flags"][others], ref_bad["flags"][others])
+    assert len(targets) == 3
+
+
+def test_group_select_ranks_past_2_32():
+    """The group P95 radix selection keeps the residual rank as a full u64:
+    synthetic histograms with 6e9 and 5e9 completions (far past 2^32), one
+    resolved at level 1, one through the overflow levels 1-3."""
+    G, B = 2, es.ES_HIST_BINS
+    counts = torch.zeros(G * es.ES_NGSTAT, dtype=torch.uint64, device=DEV)
+    c = np.zeros((G, es.ES_NGSTAT), np.int64)
+    c[0, 3], c[1, 3] = 6_000_000_000, 5_000_000_000
+    counts.copy_(torch.from_numpy(c.reshape(-1)).view(torch.uint64))
+    state = torch.zeros(2 * G, dtype=torch.uint64, device=DEV)
+
+    def hist(entries):
+        h = np.zeros((G, B), np.int64)
+        for g, b, v in entries:
+            h[g, b] = v
+        return torch.from_numpy(h.reshape(-1)).view(torch.uint64).to(DEV)
+
+    # level 0: group 0 rank ceil(0.95*6e9)=5.7e9 -> coarse bin 20 (after 5e9 in bin 10), residual 0.7e9;
+    # group 1: everything in the overflow bin 4095, rank 4.75e9
+    es.es_group_p95_select(G, 0, counts, hist([(0, 10, 5_000_000_000), (0, 20, 1_000_000_000),
+                                              (1, 4095, 5_000_000_000)]), state)
+    # level 1: group 0 T & 0xFFF inside bin 20 -> residual 0.7e9 lands in bin 9 (after 0.5e9 in bin 7);
+    # group 1 T >> 20: 3e9 in bin 20, 2e9 in bin 30 -> bin 30, residual 1.75e9
+    es.es_group_p95_select(G, 1, counts, hist([(0, 7, 500_000_000), (0, 9, 500_000_000),
+                                              (1, 20, 3_000_000_000), (1, 30, 2_000_000_000)]), state)
+    # level 2 (overflow only): (T >> 8) & 0xFFF: bin 5 1e9, bin 6 1e9 -> bin 6, residual 0.75e9
+    es.es_group_p95_select(G, 2, counts, hist([(1, 5, 1_000_000_000), (1, 6, 1_000_000_000)]), state)
+    # level 3: T & 0xFF: bin 100 0.75e9, bin 200 1.25e9 -> bin 100
+    es.es_group_p95_select(G, 3, counts, hist([(1, 100, 750_000_000), (1, 200, 1_250_000_000)]), state)
+    torch.cuda.synchronize()
+    p95 = np_of(state.view(G, 2)[:, 0]).astype(np.int64)
+    assert int(p95[0]) == (20 << 12) | 9
+    assert int(p95[1]) == (((30 << 12) | 6) << 8) | 100
+
+
+def test_k2_golden_work_counters(monkeypatch):
+    """The hand-computed replays of tests/golden/work_counters.json through the
+    GPU replay (every segment width): counters, latencies and P95."""
+    from test_oracle_counters import GOLD, expected_row, golden_case
+    for lps in ["8", "16", "32"]:
+        monkeypatch.setenv("ES_LPS", lps)
+        for case in GOLD["cases"]:
+            prof, cfgs, tr = golden_case(case)
+            g = run_k2(inputs.Workload("golden", prof, cfgs, tr, 0))
+            assert np.array_equal(g["stats"][0], expected_row(case)), (lps, case["name"], g["stats"][0])
+            assert np.array_equal(g["latency"], np.asarray(case["latency"], np.uint32))
+            assert int(g["p95"][0]) == case["p95"]
+
+
+def test_full_size_cfg3_bench_config_sampled():
+    """BASELINE configs[2] (the bench headline) at full size -- 65,536 scenarios
+    x 8 DNNs x 5 exits x batch 1-32, MMPP, 9 SLOs -- in the bench's launch
+    configuration (the segment width the library picks for this batch): 512
+    scenarios spread over the batch are replayed one by one by the oracle and
+    compared element by element (counters, P95, every latency); the group
+    merge is checked against the per-scenario counters it sums (all 117
+    groups) and its P95 against the nearest-rank definition (Q15) applied to
+    the replayed latencies of three whole groups."""
+    w = inputs.workload("cfg3")
+    g = run_k2(w, full=False)
+    assert g["_code"] == 0
+    S = w.traces.n_scen
+    ids = np.unique(np.linspace(0, S - 1, 512).astype(np.int64))
+    sub = inputs.workload("cfg3", scen_ids=ids)
+    o = oracle.replay_batch(sub.profile, sub.cfgs, sub.traces, full=True, nthreads=16)
+    assert np.array_equal(g["stats"][ids], o["stats"])
+    assert np.array_equal(g["p95"][ids], o["p95"])
+    off = w.traces.arr_off
+    for j, s in enumerate(ids):
+        a, b = int(off[s * 8]), int(off[s * 8 + 8])
+        so = sub.traces.arr_off
+        assert np.array_equal(g["latency"][a:b], o["lat"][int(so[j * 8]):int(so[j * 8 + 8])]), s
+    G = inputs.n_groups("cfg3")
+    counts, p95 = es.group_merge(g["_handle"], g["_dev"], g["_out"], G, group=False)
+    cols = [0, 1, 2, 3, 4, 5, 8]
+    ref = np.zeros((G, len(cols)), np.uint64)
+    np.add.at(ref, w.traces.group_id.astype(np.int64), g["stats"][:, cols])
+    assert np.array_equal(np_of(counts), ref)
+    p95 = np_of(p95)
+    for grp in [0, 58, 116]:
+        vals = []
+        for s in np.nonzero(w.traces.group_id == grp)[0]:
+            W = w.cfgs[int(w.traces.cfg_idx[s])].warmup
+            vals.append(g["latency"][int(off[s * 8]) + W:int(off[s * 8 + 8])])
+        v = np.sort(np.concatenate(vals))
+        k = (95 * v.size + 99) // 100
+        assert int(p95[grp]) == int(v[k - 1]), grp
