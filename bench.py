@@ -39,7 +39,10 @@ def parse():
     ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--workload", default="cfg2", choices=sorted(PER_GPU))
+    ap.add_argument("--workload", default="cfg3", choices=sorted(PER_GPU))
+    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
+                    help="weak: S scenarios per GPU; strong: S scenarios in total, split over the GPUs")
+    ap.add_argument("--no-extra", action="store_true", help="skip the cfg2 line of the default cfg3 run")
     ap.add_argument("--scenarios", type=int, default=0, help="scenarios per GPU (default: PER_GPU[workload])")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
@@ -267,6 +270,30 @@ def run_reference(args, rank, world):
     print(json.dumps(line), flush=True)
 
 
+def init_dist(dev, world):
+    """One process per GPU; the NCCL process group is created at every N
+    (N = 1 included), so the group merge's all_reduce always runs through NCCL."""
+    import socket
+    import torch.distributed as dist
+    if "MASTER_ADDR" not in os.environ:  # plain `python bench.py` (N = 1, no torchrun)
+        with socket.socket() as so:
+            so.bind(("127.0.0.1", 0))
+            port = so.getsockname()[1]
+        os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK="0", WORLD_SIZE="1")
+    dist.init_process_group("nccl", device_id=dev)
+    return dist.group.WORLD
+
+
+def cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return None
+
+
 def main():
     args = parse()
     rank, world, local = dist_env()
@@ -281,34 +308,43 @@ def main():
 
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    pg = None
-    if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
-        pg = dist.group.WORLD
+    pg = init_dist(dev, world)
     import inputs
 
-    w, S = rank_workload(args.workload, rank, args.scenarios)
+    # weak scaling (default): each rank replays its own S-scenario batch of the
+    # config's sequence; strong: a fixed S-scenario batch split over the ranks
+    S_cfg = args.scenarios or PER_GPU[args.workload]
+    if args.scaling == "strong":
+        ids = engine.shard_ids(S_cfg, rank, world)
+        w = inputs.workload(args.workload, scen_ids=ids)
+        S = int(ids.size)
+    else:
+        w, S = rank_workload(args.workload, rank, args.scenarios)
     G = inputs.n_groups(args.workload)
     h = es.es_load_profile(w.profile, w.cfgs, device=local)
     dtr = engine.upload_traces(w.traces, dev)
     total = int(w.traces.arrival.size)
     out = es.alloc_replay_out(h, S, total, dev, full=False, p95=True)
     stream = torch.cuda.current_stream()
-    ev_k2 = []
+    ev = {"k2": [], "k3": [], "merge": []}
 
     def step(record):
+        e = [torch.cuda.Event(enable_timing=True) for _ in range(4)] if record else None
         if record:
-            a = torch.cuda.Event(enable_timing=True)
-            b = torch.cuda.Event(enable_timing=True)
-            a.record(stream)
+            e[0].record(stream)
         es.es_replay_traces(h, dtr["arr_off"], dtr["arrival"], dtr["cfg_idx"], dtr["group_id"], out=out,
                             full=False, p95=False, stream=stream)
         if record:
-            b.record(stream)
-            ev_k2.append((a, b))
+            e[1].record(stream)
         # K3 (per-scenario P95) fused with the level-0 group histogram, then the
-        # all_reduce'd radix levels of the exact group P95
-        return engine.group_merge(h, dtr, out, G, group=pg if world > 1 else False, stream=stream, with_p95=True)
+        # NCCL all_reduce'd radix levels of the exact group P95 (engine.group_merge)
+        counts, p95g = engine.group_merge(h, dtr, out, G, group=pg, stream=stream, with_p95=True,
+                                          events=e[2:] if record else None)
+        if record:
+            ev["k2"].append((e[0], e[1]))
+            ev["k3"].append((e[1], e[2]))
+            ev["merge"].append((e[2], e[3]))
+        return counts, p95g
 
     for _ in range(max(args.warmup, 1)):
         counts, p95g = step(False)
@@ -332,8 +368,7 @@ def main():
         sampler.start()
         time.sleep(0.3)
     l0 = h.launches
-    if world > 1:
-        dist.barrier()
+    dist.barrier()
     torch.cuda.synchronize()
     t0 = torch.cuda.Event(enable_timing=True)
     t1 = torch.cuda.Event(enable_timing=True)
@@ -342,45 +377,46 @@ def main():
         step(True)
     t1.record(stream)
     torch.cuda.synchronize()
-    if world > 1:
-        dist.barrier()
+    dist.barrier()
     clocks = sampler.stop() if sampler else None
     launches = h.launches - l0 + 4 * args.steps  # + the four group-select kernels per step
     ms = t0.elapsed_time(t1)
-    k2_ms = [a.elapsed_time(b) for a, b in ev_k2]
+    kms = {k: statistics.mean(a.elapsed_time(b) for a, b in v) for k, v in ev.items()}
     tt = torch.tensor([ms, float(decisions_rank), float(cand_rank)], dtype=torch.float64, device=dev)
-    if world > 1:
-        mx = tt[:1].clone()
-        dist.all_reduce(mx, op=dist.ReduceOp.MAX)
-        sm = tt[1:].clone()
-        dist.all_reduce(sm, op=dist.ReduceOp.SUM)
-        ms_max, dec_all, cand_all = float(mx[0]), float(sm[0]), float(sm[1])
-    else:
-        ms_max, dec_all, cand_all = ms, float(decisions_rank), float(cand_rank)
+    mx = tt[:1].clone()
+    dist.all_reduce(mx, op=dist.ReduceOp.MAX)
+    sm = tt[1:].clone()
+    dist.all_reduce(sm, op=dist.ReduceOp.SUM)
+    ms_max, dec_all, cand_all = float(mx[0]), float(sm[0]), float(sm[1])
     value = dec_all * args.steps / (ms_max / 1e3)
 
     # ---------------- roofline of the dominant kernel (K2) -- issue/ALU bound
     hbm, sm_max, src = peaks()
-    k2_avg_s = statistics.mean(k2_ms) / 1e3
+    k2_avg_s = kms["k2"] / 1e3
     ops = alg_ops(ssum, total, w.profile.E)
-    peak_ops = 148 * 128 * sm_max * 1e6  # INT32 lanes x clock (B300_MICROARCH alu+fma pipes)
+    peak_ops = 148 * 128 * sm_max * 1e6  # 148 SMs x 4 schedulers x 32 lanes x clock (SURVEY 8(d) issue peak)
     achieved = ops / k2_avg_s
     alg_bytes = 4 * total + 4 * total + 8 * 11 * S + 8 * (S * w.profile.M + 1)
     roof = {"bound": "alu", "achieved": achieved / 1e9, "peak": peak_ops / 1e9, "unit": "Gop/s",
-            "frac": achieved / peak_ops, "traffic": ncu_traffic("k2_replay"), "kernel": "k2_replay",
-            "k2_ms": statistics.mean(k2_ms), "k2_share_of_step": statistics.mean(k2_ms) / (ms / args.steps),
-            "peak_source": f"148 SM x 128 INT32 lanes x {sm_max:.0f} MHz ({src} sm_max)",
+            "frac": achieved / peak_ops, "traffic": ncu_traffic("k2_replay_" + args.workload),
+            "kernel": "k2_replay", "k2_ms": kms["k2"], "k2_share_of_step": kms["k2"] / (ms / args.steps),
+            "peak_source": f"148 SM x 4 SMSP x 32 lanes x {sm_max:.0f} MHz ({src} sm_max): SURVEY 8(d)'s issue "
+                           "peak in thread-instruction units",
             "alg_ops_per_launch": ops,
-            "issue_view": {"ncu": ncu_issue("k2_replay"), "decisions_per_launch": decisions_rank,
-                           "note": "latency-bound chain per scenario; smsp__issue_active from profiles/"},
+            "alg_ops_model": "DESIGN.md 6: 3 per Eq. 4 term + 7 per live task + 2 per examined (m,e) cell + 7 per "
+                             "candidate + 4 per request + 2 per decision, counted exactly by the kernel",
             "hbm_view": {"alg_bytes_per_launch": alg_bytes, "achieved_gbs": alg_bytes / k2_avg_s / 1e9,
                          "peak_gbs": hbm, "frac": alg_bytes / k2_avg_s / 1e9 / hbm}}
+    k3_bytes = 4 * total + 8 * 11 * S  # K3 reads every latency once (+ the per-scenario counters)
+    kernels = {"k2_ms": kms["k2"], "k3_ms": kms["k3"], "merge_ms": kms["merge"],
+               "k3_gbs": k3_bytes / (kms["k3"] / 1e3) / 1e9,
+               "merge_note": "group levels 1-3 (es_group_hist + NCCL all_reduce + es_group_p95_select)"}
 
     # chain view: K2 is bound by its longest dependent chain of decisions; the
     # longest scenario replayed alone on the GPU is that chain's latency floor
     if not args.ncu:
         s_max = int(np.argmax(st[:, 0]))
-        w1 = inputs.workload(args.workload, scen_ids=np.array([rank * S + s_max], np.int64))
+        w1 = inputs.workload(args.workload, scen_ids=np.array([int(w.traces.scen_ids[s_max])], np.int64))
         d1 = engine.upload_traces(w1.traces, dev)
         o1 = es.alloc_replay_out(h, 1, int(w1.traces.arrival.size), dev, full=False, p95=False)
         t1 = []
@@ -395,88 +431,135 @@ def main():
                 t1.append(a1.elapsed_time(b1))
         alone = statistics.median(t1)
         roof["chain_view"] = {"longest_chain_decisions": int(st[s_max, 0]), "alone_ms": alone,
-                              "k2_ms": statistics.mean(k2_ms), "frac": alone / statistics.mean(k2_ms),
+                              "k2_ms": kms["k2"], "frac": alone / kms["k2"],
+                              "cycles_per_decision_alone": alone * 1e-3 * sm_max * 1e6 / max(1, int(st[s_max, 0])),
                               "note": "longest scenario replayed alone = the batch's latency floor; frac = floor / K2"}
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "u32", "data": "synthetic",
+            "scaling": args.scaling, "vs_baseline": None, "dtype": "u32", "data": "synthetic",
             "config": {"workload": DESC[args.workload], "scenarios_per_gpu": S, "requests_per_gpu": total, "groups": G,
                        "l2": f"inputs larger than L2 ({4 * total / 1e6:.0f} MB arrivals/GPU > 126 MB)"
                              if 4 * total > 126e6 else f"inputs fit L2 ({4 * total / 1e6:.1f} MB arrivals/GPU)",
-                       "parallelism": f"scenario-sharded x{world}, NCCL all_reduce of group histograms"},
+                       "parallelism": f"scenario-sharded x{world} ({args.scaling} scaling), NCCL all_reduce of "
+                                      "group counters and histograms"},
             "scored_candidates_per_s": cand_all * args.steps / (ms_max / 1e3),
-            "decisions_per_step": dec_all, "gpu_launches": launches, "roofline": roof}
+            "decisions_per_step": dec_all, "gpu_launches": launches, "kernels": kernels, "roofline": roof}
     if clocks:
         line["clocks"] = clocks
 
-    # ---------------- e2e through the host-buffer C-ABI call (rank-local)
+    # ---------------- e2e: the same step through the public host-memory API
+    # (engine.replay_group_stats_host: pinned H2D of every step's traces,
+    # K2 + K3 + the NCCL group merge, D2H of counters and P95s)
     if not args.no_e2e and not args.ncu:
         pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory()
         tr = w.traces
-        hin = [pin(tr.arr_off), pin(tr.arrival), pin(tr.cfg_idx), pin(tr.group_id)]
-        ho = {"stats": pin(np.zeros((S, es.ES_NSTAT), np.uint64)), "p95": pin(np.zeros(S, np.uint32)),
-              "dec_cap": 0}
-        for _ in range(2):
-            es.es_replay_traces_host(h, *hin, out=ho, stream=stream)
-        if world > 1:
-            dist.barrier()
+        hin = {"arr_off": pin(tr.arr_off.view(np.int64)).view(torch.uint64),
+               "arrival": pin(tr.arrival.view(np.int32)).view(torch.uint32),
+               "cfg_idx": pin(tr.cfg_idx.view(np.int16)).view(torch.uint16),
+               "group_id": pin(tr.group_id.view(np.int32)).view(torch.uint32)}
+        mk = lambda: {"stats": torch.empty((S, es.ES_NSTAT), dtype=torch.uint64).pin_memory(),
+                      "p95": torch.empty(S, dtype=torch.uint32).pin_memory(),
+                      "counts": torch.empty((G, es.ES_NGSTAT), dtype=torch.uint64).pin_memory(),
+                      "gp95": torch.empty(G, dtype=torch.uint64).pin_memory()}
         n_e2e = max(3, min(args.steps, 20))
-        # every step copies its own inputs in and its results out; the pipelined
-        # call overlaps step k+1's input copy with step k's replay
-        batches = [(*hin, ho) for _ in range(n_e2e)]
-        es.es_replay_traces_host_pipelined(h, batches[:2], stream=stream)
-        a = time.perf_counter()
+        houts = [mk(), mk()]
+        engine.replay_group_stats_host(h, [(hin, houts[0])], G, group=pg, stream=stream)  # warm
+        dist.barrier()
+        torch.cuda.synchronize()
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
+        a = time.perf_counter()
         e0.record(stream)
-        es.es_replay_traces_host_pipelined(h, batches, stream=stream)
+        engine.replay_group_stats_host(h, [(hin, houts[k & 1]) for k in range(n_e2e)], G, group=pg, stream=stream)
         e1.record(stream)
         torch.cuda.synchronize()
         e_ms = e0.elapsed_time(e1)
         wall_ms = (time.perf_counter() - a) * 1e3
         et = torch.tensor([max(e_ms, wall_ms)], dtype=torch.float64, device=dev)
-        if world > 1:
-            dist.all_reduce(et, op=dist.ReduceOp.MAX)
+        dist.all_reduce(et, op=dist.ReduceOp.MAX)
         e2e_v = dec_all * n_e2e / (float(et[0]) / 1e3)
-        h2d = sum(int(x.numel() * x.element_size()) for x in hin)
-        d2h = int(ho["stats"].numel() * 8 + ho["p95"].numel() * 4)
-        assert np.array_equal(ho["stats"].numpy(), st)
+        h2d = sum(int(x.numel() * x.element_size()) for x in hin.values())
+        d2h = sum(int(x.numel() * x.element_size()) for x in houts[0].values())
+        assert np.array_equal(houts[0]["stats"].numpy(), st)
+        assert np.array_equal(houts[0]["counts"].numpy(), counts.cpu().numpy())
+        assert np.array_equal(houts[0]["gp95"].numpy(), p95g.cpu().numpy())
         line["e2e"] = {"value": e2e_v, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                        "steps": n_e2e,
-                       "call": "es_replay_traces_host_pipelined (pinned host in/out per step, K2+K3; step k+1's "
-                               "H2D overlaps step k's replay)"}
+                       "call": "engine.replay_group_stats_host (pinned host traces in, per-scenario counters + P95 "
+                               "and group counters + P95 out, every step; K2 + K3 + NCCL group merge; step k+1's "
+                               "H2D overlaps step k)"}
 
     # ---------------- K1: independent snapshot scoring, the HBM-streaming form
     if not args.no_k1 and not args.ncu:
         line["k1"] = bench_k1(es, h_cache={}, dev=dev, stream=stream, rank=rank)
 
+    # ---------------- the other configs' headline lines (K2 + K3 + merge per step)
+    if args.workload == "cfg3" and not args.no_extra and not args.ncu:
+        line["cfg2"] = bench_extra("cfg2", es, engine, dev, stream, pg, rank)
+
     # ---------------- CPU baseline: the oracle on the host cores (rank 0, N=1)
     if rank == 0 and world == 1 and not args.no_cpu_baseline and not args.ncu:
-        import oracle
-        cores = os.cpu_count() or 1
-        # bounded sample: the first k scenarios of the batch, <= ~50M requests
-        per = total / S
-        k = S if total <= 50e6 else max(1, int(50e6 // per))
-        ws = w if k == S else inputs.workload(args.workload, scen_ids=np.arange(k, dtype=np.int64))
-        reps = 0
-        t = time.perf_counter()
-        while True:  # >= ~1 s wall (~16 s of CPU work on 16 cores)
-            o = oracle.replay_batch(ws.profile, ws.cfgs, ws.traces, full=False, nthreads=cores)
-            reps += 1
-            if time.perf_counter() - t > 1.0:
-                break
-        dt = (time.perf_counter() - t) / reps
-        assert np.array_equal(o["stats"], st[:k]), "oracle and GPU disagree on the bench batch"
-        assert np.array_equal(o["p95"], out["p95"].cpu().numpy()[:k])
-        what = f"the full {S}-scenario bench batch" if k == S else f"the first {k} of the {S} bench scenarios"
-        line["cpu_baseline"] = {"value": int(o["stats"][:, 0].sum()) / dt, "unit": UNIT, "cores": cores,
-                                "kind": "oracle",
-                                "sample": f"{what} (rank 0), {reps} replay(s), {dt:.2f} s wall each on {cores} threads",
-                                "parity": f"bit-exact on all per-scenario counters and P95 of those {k} scenarios"}
+        line["cpu_baseline"] = cpu_baseline(args, w, S, total, st, out)
     if rank == 0:
         print(json.dumps(line), flush=True)
-    if world > 1:
-        dist.destroy_process_group()
+    dist.destroy_process_group()
+
+
+def bench_extra(name, es, engine, dev, stream, pg, rank, steps=20):
+    """Another config's step (K2 + K3 + NCCL group merge), device-timed."""
+    import torch
+    import inputs
+    w, S = rank_workload(name, rank)
+    G = inputs.n_groups(name)
+    h = es.es_load_profile(w.profile, w.cfgs, device=dev.index)
+    d = engine.upload_traces(w.traces, dev)
+    o = es.alloc_replay_out(h, S, int(w.traces.arrival.size), dev, full=False, p95=True)
+    for _ in range(3):
+        engine.replay_group_stats(h, d, G, group=pg, stream=stream, out=o)
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record(stream)
+    for _ in range(steps):
+        engine.replay_group_stats(h, d, G, group=pg, stream=stream, out=o)
+    b.record(stream)
+    torch.cuda.synchronize()
+    ms = a.elapsed_time(b) / steps
+    dec = float(o["stats"][:, 0].sum().item())
+    return {"workload": DESC[name], "value": dec / (ms / 1e3), "unit": UNIT, "ms_per_step": ms, "steps": steps,
+            "decisions_per_step": dec}
+
+
+def cpu_baseline(args, w, S, total, st, out):
+    """The oracle as it stands on the host cores: all cores on a bounded sample
+    (bit-exact check against the GPU on it) and one core on a smaller one."""
+    import inputs
+    import oracle
+    cores = os.cpu_count() or 1
+    per = total / S
+    k = S if total <= 50e6 else max(1, int(50e6 // per))  # <= ~50M requests
+    ws = w if k == S else inputs.workload(args.workload, scen_ids=w.traces.scen_ids[:k])
+    reps = 0
+    t = time.perf_counter()
+    while True:  # >= ~1 s wall (~16 s of CPU work on 16 cores)
+        o = oracle.replay_batch(ws.profile, ws.cfgs, ws.traces, full=False, nthreads=cores)
+        reps += 1
+        if time.perf_counter() - t > 1.0:
+            break
+    dt = (time.perf_counter() - t) / reps
+    assert np.array_equal(o["stats"], st[:k]), "oracle and GPU disagree on the bench batch"
+    assert np.array_equal(o["p95"], out["p95"].cpu().numpy()[:k])
+    k1 = max(1, min(k, int(2e6 // per)))  # single thread: ~2M requests
+    w1 = inputs.workload(args.workload, scen_ids=w.traces.scen_ids[:k1])
+    t = time.perf_counter()
+    o1 = oracle.replay_batch(w1.profile, w1.cfgs, w1.traces, full=False, nthreads=1)
+    dt1 = time.perf_counter() - t
+    what = f"the full {S}-scenario bench batch" if k == S else f"the first {k} of the {S} bench scenarios"
+    return {"value": int(o["stats"][:, 0].sum()) / dt, "unit": UNIT, "cores": cores, "kind": "oracle",
+            "cpu_model": cpu_model(),
+            "sample": f"{what} (rank 0), {reps} replay(s), {dt:.2f} s wall each on {cores} threads",
+            "parity": f"bit-exact on all per-scenario counters and P95 of those {k} scenarios",
+            "single_thread": {"value": int(o1["stats"][:, 0].sum()) / dt1, "unit": UNIT, "cores": 1,
+                              "sample": f"the first {k1} scenarios, {dt1:.2f} s on 1 thread"}}
 
 
 if __name__ == "__main__":

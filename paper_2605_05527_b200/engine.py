@@ -35,7 +35,7 @@ def _all_reduce(x, group):
     dist.all_reduce(x.view(torch.int64), op=dist.ReduceOp.SUM, group=group)
 
 
-def group_merge(prof, dtr, out, n_groups, group=None, stream=None, with_p95=False):
+def group_merge(prof, dtr, out, n_groups, group=None, stream=None, with_p95=False, events=None):
     """Exact per-group counters and nearest-rank P95 across all ranks.
 
     dtr: uploaded traces of this rank's scenarios; out: this rank's replay
@@ -54,6 +54,8 @@ def group_merge(prof, dtr, out, n_groups, group=None, stream=None, with_p95=Fals
     state = torch.zeros(2 * G, dtype=torch.uint64, device=dev)
     es_scen_stats(prof, dtr["arr_off"], dtr["arrival"], out, G, counts, hist, dtr["cfg_idx"], dtr["group_id"],
                   p95=with_p95, stream=stream)
+    if events:  # timing marks: after K3 + level 0, after the last level
+        events[0].record(stream)
     _all_reduce(buf, group)
     es_group_p95_select(G, 0, counts, hist, state, stream)
     for level in (1, 2, 3):
@@ -61,6 +63,8 @@ def group_merge(prof, dtr, out, n_groups, group=None, stream=None, with_p95=Fals
                       dtr["group_id"], stream)
         _all_reduce(hist, group)
         es_group_p95_select(G, level, counts, hist, state, stream)
+    if events:
+        events[1].record(stream)
     return counts.view(G, ES_NGSTAT), state.view(G, 2)[:, 0]
 
 
@@ -89,3 +93,50 @@ def weak_ids(per_rank, rank):
 
 # group-P95 radix levels (normal path): level 0 coarse min(T >> 12, 4095), level 1 T & 0xFFF
 COARSE_SHIFT, COARSE_OVF = 12, 4095
+
+
+def replay_group_stats_host(prof, host_batches, n_groups, group=None, stream=None):
+    """End-to-end form of replay_group_stats over host batches (the call a user
+    with traces in host memory makes).  host_batches: list of (hin, hout) with
+    hin = {"arr_off", "arrival", "cfg_idx", "group_id"} pinned host tensors and
+    hout = {"stats", "p95", "counts", "gp95"} pinned host tensors.  Per batch:
+    the inputs go host -> device on a copy stream into one of two device
+    buffers (batch k+1's copy overlaps batch k's replay), then K2 + K3 + the
+    group merge (NCCL all_reduce across ranks when `group` is a process group)
+    run on `stream`, and the per-scenario counters, per-scenario P95, group
+    counters and group P95 come back device -> host.  Synchronises `stream`."""
+    import torch
+    from . import alloc_replay_out, es_replay_traces
+    if not host_batches:
+        return
+    stream = stream or torch.cuda.current_stream()
+    dev = stream.device
+    hin0 = host_batches[0][0]
+    bufs = [{k: torch.empty_like(v, device=dev) for k, v in hin0.items()} for _ in range(2)]
+    n = (hin0["arr_off"].numel() - 1) // prof.M
+    out = alloc_replay_out(prof, n, hin0["arrival"].numel(), dev, full=False, p95=True)
+    copy = torch.cuda.Stream(device=dev)
+    ev_copied = [torch.cuda.Event(), torch.cuda.Event()]
+    ev_done = [torch.cuda.Event(), torch.cuda.Event()]
+    copy.wait_stream(stream)
+    for k, (hin, hout) in enumerate(host_batches):
+        b = k & 1
+        d = bufs[b]
+        assert all(hin[x].shape == hin0[x].shape for x in hin0), "equal batch shapes"
+        with torch.cuda.stream(copy):
+            if k >= 2:
+                copy.wait_event(ev_done[b])
+            for x in d:
+                d[x].copy_(hin[x], non_blocking=True)
+            ev_copied[b].record(copy)
+        stream.wait_event(ev_copied[b])
+        with torch.cuda.stream(stream):
+            es_replay_traces(prof, d["arr_off"], d["arrival"], d["cfg_idx"], d["group_id"], out=out, full=False,
+                             p95=False, stream=stream)
+            counts, gp95 = group_merge(prof, d, out, n_groups, group=group, stream=stream, with_p95=True)
+            hout["stats"].copy_(out["stats"], non_blocking=True)
+            hout["p95"].copy_(out["p95"], non_blocking=True)
+            hout["counts"].copy_(counts, non_blocking=True)
+            hout["gp95"].copy_(gp95, non_blocking=True)
+            ev_done[b].record(stream)
+    stream.synchronize()
