@@ -291,18 +291,22 @@ __device__ __forceinline__ Cand cand_params(const Seg<LPS, MM> &sg, const SmemPr
     if (k.L >= C.x_c) k.H = 0ull;
     return k;
   }
+  // more exits than group lanes: every lane evaluates Eq. 6 for all exits of
+  // its group's model itself (E independent shared-memory loads, no ballot
+  // rounds on the decision's chain)
+  uint32_t Lv[MAXE];
 #pragma unroll
-  for (int e0 = 0; e0 < MAXE; e0 += GL) {  // compile-time trip count, E <= MAXE
-    if (e0 >= P.E) break;                 // warp-uniform
-    const int e = e0 + sg.gl;
-    bool ok = false;
-    if (e < P.E && ((mbits >> e) & 1u)) ok = (uint64_t)wmax + row[e * P.nb] <= (uint64_t)C.tau;
-    bits |= sg.gbits(__ballot_sync(FULL, ok)) << e0;
-  }
+  for (int e = 0; e < MAXE; ++e) Lv[e] = e < P.E ? row[e * P.nb] : 0xFFFFFFFFu;
+#pragma unroll
+  for (int e = 0; e < MAXE; ++e)
+    if (e < P.E && ((mbits >> e) & 1u) && (uint64_t)wmax + Lv[e] <= (uint64_t)C.tau) bits |= 1u << e;
   k.feas = bits != 0u;
   k.e = k.feas ? 31u - __clz(bits) : (uint32_t)(__ffs(mbits) - 1);
   if (fixed) k.e = fixed == 1 ? 31u - __clz(mbits) : (uint32_t)(__ffs(mbits) - 1);
-  k.L = row[k.e * P.nb];
+  k.L = Lv[0];
+#pragma unroll
+  for (int e = 1; e < MAXE; ++e)
+    if ((uint32_t)e == k.e) k.L = Lv[e];
   if (fixed) k.feas = (uint64_t)wmax + k.L <= (uint64_t)C.tau;
   k.thr = k.L < C.x_c ? C.x_c - k.L : 0u;
   k.H = k.L < C.x_c ? reinterpret_cast<const uint64_t *>(P.hb + C.off_H)[((size_t)gg * P.E + k.e) * P.nb + bi]

@@ -91,6 +91,7 @@ __global__ void ES_K2_BOUNDS k2_replay(const uint8_t *__restrict__ gimg, ImgLayo
   uint64_t base0 = 0, qb = 0;
   const uint32_t *Aq = a.arrival;
   uint32_t n = 0, head = 0, tail = 0, live = 0, last = 0, next_arr = 0xFFFFFFFFu;
+  uint32_t win = 0xFFFFFFFFu;  // arrival at position tail + gl (admission window, loaded ahead)
   uint32_t t = 0, total = 0, served = 0, seq = 0, status = 0, iters = 0;
   uint64_t decisions = 0, candidates = 0, infeasible = 0;
   // lane-local counters (reduced once per scenario)
@@ -125,6 +126,7 @@ __global__ void ES_K2_BOUNDS k2_replay(const uint8_t *__restrict__ gimg, ImgLayo
         }
         Aq = a.arrival + qb;
         if (n_new) a0 = ldg_u32(Aq);
+        win = (uint32_t)sg.gl < n_new ? ldg_u32(Aq + sg.gl) : 0xFFFFFFFFu;
       }
       const uint32_t tot = sg.sum(sg.gl == 0 ? n_new : 0u);
       const uint32_t t0 = sg.vmin(a0);
@@ -153,11 +155,14 @@ __global__ void ES_K2_BOUNDS k2_replay(const uint8_t *__restrict__ gimg, ImgLayo
       // a2: admission (every arrival with a <= t)
       const bool pre_ok = run && head < tail;
       const uint32_t ahead_pre = pre_ok ? ldg_u32(Aq + head) : 0u;  // head arrival, issued early
-      bool more = true;
+      bool more = true, first = true;
       while (more) {
         const uint32_t idx = tail + sg.gl;
         const bool valid = run && idx < n;
-        const uint32_t v = valid ? ldg_u32(Aq + idx) : 0xFFFFFFFFu;
+        // first round: the register window loaded at the end of the previous
+        // admission (its load is off this decision's chain)
+        const uint32_t v = !valid ? 0xFFFFFFFFu : first ? win : ldg_u32(Aq + idx);
+        first = false;
         uint32_t prev = __shfl_up_sync(FULL, v, 1, GL);
         if (sg.gl == 0) prev = last;
         const bool ok = valid && v <= t;
@@ -174,6 +179,8 @@ __global__ void ES_K2_BOUNDS k2_replay(const uint8_t *__restrict__ gimg, ImgLayo
         }
         more = __any_sync(FULL, run && status == ES_OK && cnt == (uint32_t)GL);
       }
+      // the next decision's first admission round reads this window
+      if (run && tail + sg.gl < n) win = ldg_u32(Aq + tail + sg.gl);
       // keep the next PF_LINES 128-byte lines of this model's arrivals in L1
       // (the admission loads above are the head of the per-decision chain)
       if (run && sg.gl < PF_LINES) {
