@@ -33,6 +33,15 @@ METRIC = "scheduling decisions/sec (stability-score evals)"
 UNIT = "decisions/s"
 
 
+_OUT_FD = None
+
+
+def emit(line):
+    """The one JSON line on stdout.  Everything else the process (or NCCL's
+    version banner) writes to fd 1 is redirected to stderr by main()."""
+    os.write(_OUT_FD if _OUT_FD is not None else 1, (json.dumps(line) + "\n").encode())
+
+
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -267,7 +276,7 @@ def run_reference(args, rank, world):
             "config": {"workload": DESC[args.workload], "scenarios_per_step": chunk},
             "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": sample},
             "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
-    print(json.dumps(line), flush=True)
+    emit(line)
 
 
 def init_dist(dev, world):
@@ -295,7 +304,11 @@ def cpu_model():
 
 
 def main():
+    global _OUT_FD
     args = parse()
+    sys.stdout.flush()
+    _OUT_FD = os.dup(1)
+    os.dup2(2, 1)  # stray prints (NCCL's banner included) go to stderr
     rank, world, local = dist_env()
     if args.impl == "reference":
         run_reference(args, rank, world)
@@ -501,7 +514,7 @@ def main():
     if rank == 0 and world == 1 and not args.no_cpu_baseline and not args.ncu:
         line["cpu_baseline"] = cpu_baseline(args, w, S, total, st, out)
     if rank == 0:
-        print(json.dumps(line), flush=True)
+        emit(line)
     dist.destroy_process_group()
 
 

@@ -19,6 +19,8 @@
 // Levels 2-3 are no-ops for groups resolved at level 1 (the common case).
 #include <cuda_runtime.h>
 
+#include <algorithm>
+
 #include "es_internal.cuh"
 
 namespace es {
@@ -253,10 +255,52 @@ struct GroupArgs {
   uint64_t *hist;         // [G][4096]
 };
 
-// levels 1-3: histogram of the digit selected by the group's state
-__global__ void __launch_bounds__(NT) k_group_level(GroupArgs a) {
+// level-1..3 digit of latency v for a group in state (ovf, prefix); false if
+// v does not match the prefix selected so far
+__device__ __forceinline__ bool level_digit(uint32_t v, int level, bool ovf, uint32_t prefix, uint32_t &bin) {
+  if (!ovf) {  // level 1, normal: exact value inside the coarse bin
+    bin = v & 0xFFFu;
+    return (v >> 12) == prefix;
+  }
+  if (level == 1) {
+    bin = v >> 20;
+    return (v >> 12) >= COARSE_OVF;
+  }
+  if (level == 2) {
+    bin = (v >> 8) & 0xFFFu;
+    return (v >> 12) >= COARSE_OVF && (v >> 20) == prefix;
+  }
+  bin = v & 0xFFu;
+  return (v >> 12) >= COARSE_OVF && (v >> 8) == prefix;
+}
+
+// levels 1-3: histogram of the digit selected by each group's state.  The
+// scenarios come grouped (a device counting sort by group id, `order`), each
+// CTA streams a contiguous run of them -- 16-byte loads of the latencies --
+// into one shared-memory histogram that is flushed to the group's global
+// histogram only when the run moves to another group (or ends).
+__global__ void __launch_bounds__(NT) k_group_level(GroupArgs a, const uint32_t *order, int64_t per_cta) {
   __shared__ uint32_t hist[BINS];
-  for (int64_t s = blockIdx.x; s < a.n_scen; s += gridDim.x) {
+  for (int i = threadIdx.x; i < BINS; i += NT) hist[i] = 0u;
+  __syncthreads();
+  const int64_t lo = (int64_t)blockIdx.x * per_cta, hi = ::min(lo + per_cta, a.n_scen);
+  uint32_t cur = 0xFFFFFFFFu;  // group whose counts hist holds
+  bool dirty = false;
+  auto flush = [&]() {
+    __syncthreads();
+    if (dirty) {
+      unsigned long long *gh = reinterpret_cast<unsigned long long *>(a.hist + (uint64_t)cur * BINS);
+      for (int i = threadIdx.x; i < BINS; i += NT)
+        if (hist[i]) {
+          atomicAdd(gh + i, (unsigned long long)hist[i]);
+          hist[i] = 0u;
+        }
+    }
+    dirty = false;
+    __syncthreads();
+  };
+  for (int64_t j = lo; j < hi; ++j) {
+    const int64_t s = order[j];
     const uint64_t *st = a.stats + s * ES_NSTAT;
     if (st[ES_ST_STATUS] != 0ull) continue;
     const uint32_t g = a.group_id ? a.group_id[s] : 0u;
@@ -272,37 +316,71 @@ __global__ void __launch_bounds__(NT) k_group_level(GroupArgs a) {
     const uint64_t base = a.arr_off[s * a.M];
     const uint64_t total = a.arr_off[s * a.M + a.M] - base;
     if (total <= W) continue;
-    const uint32_t n = (uint32_t)(total - W);
-    const uint32_t *src = a.lat + base + W;
-    for (int i = threadIdx.x; i < BINS; i += NT) hist[i] = 0u;
-    __syncthreads();
-    for (uint32_t i0 = 0; i0 < n; i0 += NT) {
-      const uint32_t i = i0 + threadIdx.x;
-      const uint32_t v = i < n ? src[i] : 0u;
-      uint32_t bin = 0;
-      bool take = false;
-      if (i < n) {
-        if (!ovf) {  // level 1, normal: exact value inside the coarse bin
-          take = (v >> 12) == prefix;
-          bin = v & 0xFFFu;
-        } else if (a.level == 1) {
-          take = (v >> 12) >= COARSE_OVF;
-          bin = v >> 20;
-        } else if (a.level == 2) {
-          take = (v >> 12) >= COARSE_OVF && (v >> 20) == prefix;
-          bin = (v >> 8) & 0xFFFu;
-        } else {
-          take = (v >> 12) >= COARSE_OVF && (v >> 8) == prefix;
-          bin = v & 0xFFu;
-        }
-      }
-      if (take) atomicAdd(&hist[bin], 1u);
+    if (g != cur) {  // uniform across the CTA
+      flush();
+      cur = g;
     }
+    dirty = true;
+    // latencies [b0, b1): scalar head up to 16-byte alignment, uint4 body, scalar tail
+    const uint64_t b0 = base + W, b1 = base + total;
+    const uint64_t h1 = ::min((uint64_t)((b0 + 3u) & ~3ull), b1), t0 = ::max((uint64_t)(b1 & ~3ull), h1);
+    uint32_t bin;
+    if (threadIdx.x < h1 - b0 && level_digit(a.lat[b0 + threadIdx.x], a.level, ovf, prefix, bin))
+      atomicAdd(&hist[bin], 1u);
+    if (threadIdx.x < b1 - t0 && level_digit(a.lat[t0 + threadIdx.x], a.level, ovf, prefix, bin))
+      atomicAdd(&hist[bin], 1u);
+    const uint4 *body = reinterpret_cast<const uint4 *>(a.lat + h1);
+    const uint64_t nv = (t0 - h1) / 4u;
+    for (uint64_t i = threadIdx.x; i < nv; i += NT) {
+      const uint4 q = __ldcs(body + i);  // streamed once per level: do not keep it in L1/L2
+      if (level_digit(q.x, a.level, ovf, prefix, bin)) atomicAdd(&hist[bin], 1u);
+      if (level_digit(q.y, a.level, ovf, prefix, bin)) atomicAdd(&hist[bin], 1u);
+      if (level_digit(q.z, a.level, ovf, prefix, bin)) atomicAdd(&hist[bin], 1u);
+      if (level_digit(q.w, a.level, ovf, prefix, bin)) atomicAdd(&hist[bin], 1u);
+    }
+  }
+  flush();
+}
+
+// counting sort of the scenarios by group id (the grouped order k_group_level streams)
+__global__ void k_group_count(int64_t n_scen, const uint32_t *group_id, uint32_t n_groups, unsigned *cnt) {
+  for (int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; s < n_scen; s += (int64_t)gridDim.x * blockDim.x) {
+    const uint32_t g = group_id ? group_id[s] : 0u;
+    atomicAdd(cnt + (g < n_groups ? g : n_groups), 1u);  // bucket n_groups: out-of-range ids
+  }
+}
+
+__global__ void k_group_scan(uint32_t nb, unsigned *cnt) {  // one CTA: exclusive scan in place (nb buckets)
+  __shared__ unsigned carry;
+  if (threadIdx.x == 0) carry = 0u;
+  __syncthreads();
+  for (uint32_t b0 = 0; b0 < nb; b0 += NT) {
+    const uint32_t i = b0 + threadIdx.x;
+    const unsigned v = i < nb ? cnt[i] : 0u;
+    unsigned x = v;
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const unsigned y = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= o) x += y;
+    }
+    __shared__ unsigned ws[NW];
+    if (lane == 31) ws[wid] = x;
     __syncthreads();
-    unsigned long long *gh = reinterpret_cast<unsigned long long *>(a.hist + (uint64_t)g * BINS);
-    for (int i = threadIdx.x; i < BINS; i += NT)
-      if (hist[i]) atomicAdd(gh + i, (unsigned long long)hist[i]);
+    unsigned off = carry;
+    for (int w = 0; w < wid; ++w) off += ws[w];
+    if (i < nb) cnt[i] = off + x - v;
     __syncthreads();
+    if (threadIdx.x == NT - 1) carry = off + x;
+    __syncthreads();
+  }
+}
+
+__global__ void k_group_scatter(int64_t n_scen, const uint32_t *group_id, uint32_t n_groups, unsigned *pos,
+                                uint32_t *order) {
+  for (int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; s < n_scen; s += (int64_t)gridDim.x * blockDim.x) {
+    const uint32_t g = group_id ? group_id[s] : 0u;
+    order[atomicAdd(pos + (g < n_groups ? g : n_groups), 1u)] = (uint32_t)s;
   }
 }
 
@@ -420,6 +498,10 @@ cudaError_t launch_group_hist(const uint8_t *img, const ImgLayout &lay, const es
                               const uint64_t *state, uint64_t *hist, cudaStream_t st) {
   cudaError_t e = cudaMemsetAsync(hist, 0, (size_t)n_groups * BINS * sizeof(uint64_t), st);
   if (e != cudaSuccess) return e;
+  if (tr.n_scen >= (int64_t)0xFFFFFFFF) return cudaErrorInvalidValue;
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   GroupArgs a{};
   a.n_scen = tr.n_scen;
   a.M = lay.M;
@@ -433,9 +515,26 @@ cudaError_t launch_group_hist(const uint8_t *img, const ImgLayout &lay, const es
   a.level = level;
   a.state = state;
   a.hist = hist;
-  int64_t b = tr.n_scen < 148 * 16 ? tr.n_scen : 148 * 16;
-  k_group_level<<<(unsigned)(b < 1 ? 1 : b), NT, 0, st>>>(a);
-  return cudaGetLastError();
+  // grouped scenario order (stream-ordered scratch, per call)
+  const size_t nb = (size_t)n_groups + 1;
+  void *buf = nullptr;
+  e = cudaMallocAsync(&buf, 4 * (nb + (size_t)tr.n_scen), st);
+  if (e != cudaSuccess) return e;
+  unsigned *cnt = static_cast<unsigned *>(buf);
+  uint32_t *order = cnt + nb;
+  const int blocks = (int)std::min<int64_t>((tr.n_scen + 255) / 256, (int64_t)sms * 8);
+  e = cudaMemsetAsync(cnt, 0, 4 * nb, st);
+  if (e == cudaSuccess) {
+    k_group_count<<<blocks, 256, 0, st>>>(tr.n_scen, tr.group_id, n_groups, cnt);
+    k_group_scan<<<1, NT, 0, st>>>((uint32_t)nb, cnt);
+    k_group_scatter<<<blocks, 256, 0, st>>>(tr.n_scen, tr.group_id, n_groups, cnt, order);
+    const int64_t ctas = std::min<int64_t>(tr.n_scen, (int64_t)sms * 8);
+    const int64_t per = (tr.n_scen + ctas - 1) / ctas;
+    k_group_level<<<(unsigned)((tr.n_scen + per - 1) / per), NT, 0, st>>>(a, order, per);
+    e = cudaGetLastError();
+  }
+  const cudaError_t f = cudaFreeAsync(buf, st);
+  return e != cudaSuccess ? e : f;
 }
 
 cudaError_t launch_group_select(uint32_t n_groups, int level, const uint64_t *counts,
