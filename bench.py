@@ -409,7 +409,7 @@ def main():
     ops = alg_ops(ssum, total, w.profile.E)
     peak_ops = 148 * 128 * sm_max * 1e6  # 148 SMs x 4 schedulers x 32 lanes x clock (SURVEY 8(d) issue peak)
     achieved = ops / k2_avg_s
-    alg_bytes = 4 * total + 4 * total + 8 * 11 * S + 8 * (S * w.profile.M + 1)
+    alg_bytes = 4 * total + 4 * total + 8 * es.ES_NSTAT * S + 8 * (S * w.profile.M + 1)
     roof = {"bound": "alu", "achieved": achieved / 1e9, "peak": peak_ops / 1e9, "unit": "Gop/s",
             "frac": achieved / peak_ops, "traffic": ncu_traffic("k2_replay_" + args.workload),
             "kernel": "k2_replay", "k2_ms": kms["k2"], "k2_share_of_step": kms["k2"] / (ms / args.steps),
@@ -420,7 +420,7 @@ def main():
                              "candidate + 4 per request + 2 per decision, counted exactly by the kernel",
             "hbm_view": {"alg_bytes_per_launch": alg_bytes, "achieved_gbs": alg_bytes / k2_avg_s / 1e9,
                          "peak_gbs": hbm, "frac": alg_bytes / k2_avg_s / 1e9 / hbm}}
-    k3_bytes = 4 * total + 8 * 11 * S  # K3 reads every latency once (+ the per-scenario counters)
+    k3_bytes = 4 * total + 8 * es.ES_NSTAT * S  # K3 reads every latency once (+ the per-scenario counters)
     kernels = {"k2_ms": kms["k2"], "k3_ms": kms["k3"], "merge_ms": kms["merge"],
                "k3_gbs": k3_bytes / (kms["k3"] / 1e3) / 1e9,
                "merge_note": "group levels 1-3 (es_group_hist + NCCL all_reduce + es_group_p95_select)"}

@@ -82,6 +82,9 @@ typedef struct {
   const int32_t *batch_sizes; /* host [nb], strictly increasing, [0] == 1, <= 65535 */
   const uint32_t *latency_us; /* host [M][E][nb] row-major, L(m, e, bs[b])         */
   const uint8_t *exit_mask;   /* host [M][E] nonzero = exit allowed, or NULL = all */
+  const uint16_t *accuracy_bp; /* host [M][E] top-1 accuracy of (model, exit) in basis
+                                  points (0.01 %; Table I), <= 10000, or NULL
+                                  (= 0: the accuracy column then stays 0)            */
 } es_profile_desc;
 
 /* One scheduler configuration (SLO and knobs).  Bound to the handle at load. */
@@ -215,6 +218,11 @@ enum {
   ES_ST_SUM_LAT,       /* sum of post-warmup T, us                                  */
   ES_ST_LIVE,          /* sum over decisions of pending tasks with w < x_c (read)   */
   ES_ST_TERMS,         /* sum over decisions of live tasks x candidates (Eq. 4 terms) */
+  ES_ST_ACC_BP,        /* sum over post-warmup completions of accuracy_bp(m, e) of the
+                          exit that served them: effective accuracy = ACC_BP / COMPLETED
+                          basis points                               */
+  ES_ST_EXIT0,         /* post-warmup completions served at exit 0 (shallowest) ...   */
+  ES_ST_EXIT7 = ES_ST_EXIT0 + 7, /* ... exit 7: the exit-depth histogram (Fig. exit_depth) */
   ES_NSTAT
 };
 
@@ -277,7 +285,8 @@ ES_API es_status es_replay_traces_host_pipelined(es_profile *prof, const es_trac
 
 /* ------------------------------------------------ group merge (multi-GPU) */
 
-#define ES_NGSTAT 7 /* decisions, candidates, cells, completed, violations, infeasible, sum_lat */
+#define ES_NGSTAT 16 /* decisions, candidates, cells, completed, violations, infeasible, sum_lat,
+                        acc_bp, exit0 .. exit7 */
 #define ES_HIST_BINS 4096
 
 /*

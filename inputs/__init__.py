@@ -83,6 +83,7 @@ class Profile:
     bs: np.ndarray  # int32 [nb], strictly increasing, bs[0] == 1
     lat: np.ndarray  # uint32 [M, E, nb]
     mask: np.ndarray  # uint8 [M, E]
+    acc: np.ndarray = None  # uint16 [M, E] top-1 accuracy, basis points (Table I), or None
 
     @property
     def nb(self) -> int:
@@ -104,7 +105,27 @@ def synth_profile(M, E, bs, b_max=None, L_top=12000.0, kappa=2.0, delta=7.0, rat
                 lat[m, e, i] = math.floor(L_top * fm * fe * (1.0 + g * (int(b) - 1)) + 0.5)
     if mask is None:
         mask = np.ones((M, E), dtype=np.uint8)
-    return Profile(M=M, E=E, bs=bs, lat=lat, mask=np.asarray(mask, dtype=np.uint8))
+    return Profile(M=M, E=E, bs=bs, lat=lat, mask=np.asarray(mask, dtype=np.uint8), acc=synth_accuracy(M, E))
+
+
+# Table I: top-1 accuracy (%) on CIFAR-100 of ResNet50/101/152 at
+# layer1, layer2, layer3, final -- in basis points (0.01 %)
+TABLE_I_BP = np.array([[760, 1210, 3080, 7440], [740, 1450, 5430, 7790], [730, 1720, 4740, 7800]], np.int64)
+
+
+def synth_accuracy(M, E):
+    """Accuracy table shaped by Table I: model m takes the row of ResNet
+    (3 m) // M (lighter models first, as the latency profile orders them);
+    E = 4 uses the row as printed, other E interpolate it linearly at the exit
+    fractions e / (E - 1) over the four exits at 0, 1/3, 2/3, 1.  Data only."""
+    out = np.zeros((M, E), np.uint16)
+    xs = np.array([0.0, 1 / 3, 2 / 3, 1.0])
+    for m in range(M):
+        row = TABLE_I_BP[(3 * m) // M]
+        for e in range(E):
+            x = e / (E - 1) if E > 1 else 1.0
+            out[m, e] = row[e] if E == 4 else int(round(float(np.interp(x, xs, row.astype(np.float64)))))
+    return out
 
 
 def batch_index_of(bs, b_max):

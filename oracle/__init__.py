@@ -37,9 +37,9 @@ _lock = threading.Lock()
 _lib = None
 
 F = 28  # fractional bits of the fixed-point score (reading Q5)
-NCOL = 11
 COLS = ["decisions", "candidates", "cells", "completed", "violations", "infeasible",
-        "max_depth", "status", "sum_lat", "live", "terms"]
+        "max_depth", "status", "sum_lat", "live", "terms", "acc_bp"] + [f"exit{e}" for e in range(8)]
+NCOL = len(COLS)
 
 
 def build(force=False):
@@ -173,9 +173,11 @@ def replay_batch(prof, cfgs, traces, full=True, dec_cap=0, nthreads=1):
     bs = np.ascontiguousarray(prof.bs, np.int32)
     lat = np.ascontiguousarray(prof.lat, np.uint32)
     mask = np.ascontiguousarray(prof.mask, np.uint8)
+    acc = getattr(prof, "acc", None)
+    acc = None if acc is None else np.ascontiguousarray(acc, np.uint16)
     g = out.get
     st = lib().or_replay_batch(
-        M, prof.E, prof.nb, _p(bs), _p(lat), _p(mask), _p(tau), _p(C), _p(bm), _p(wu), _p(pol), len(cfgs),
+        M, prof.E, prof.nb, _p(bs), _p(lat), _p(mask), _p(acc), _p(tau), _p(C), _p(bm), _p(wu), _p(pol), len(cfgs),
         ctypes.c_int64(n), _p(ci), _p(arr_off), _p(arrival), _p(g("completion")), _p(g("exit")),
         _p(g("lat")), _p(out["stats"]), _p(out["p95"]), ctypes.c_int64(dec_cap), _p(g("dec_t")),
         _p(g("dec_m")), _p(g("dec_e")), _p(g("dec_B")), _p(g("dec_L")), _p(g("dec_S")),
@@ -185,7 +187,8 @@ def replay_batch(prof, cfgs, traces, full=True, dec_cap=0, nthreads=1):
     return out
 
 
-GROUP_COLS = ["decisions", "candidates", "cells", "completed", "violations", "infeasible", "sum_lat"]
+GROUP_COLS = ["decisions", "candidates", "cells", "completed", "violations", "infeasible", "sum_lat",
+              "acc_bp"] + [f"exit{e}" for e in range(8)]
 GROUP_SRC = [COLS.index(c) for c in GROUP_COLS]
 
 

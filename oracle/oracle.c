@@ -140,6 +140,7 @@ typedef struct {
   const int32_t *bs;    /* [nb] strictly increasing, bs[0] == 1 (Q8) */
   const uint32_t *lat;  /* [M][E][nb] microseconds */
   const uint8_t *mask;  /* [M][E] allowed exits, nonzero = allowed */
+  const uint16_t *acc;  /* [M][E] top-1 accuracy in basis points (Table I), or NULL */
   /* scheduler config */
   uint32_t tau, C, b_max, warmup;
   uint32_t policy; /* OR_POL_*: Algorithm 1 or one of the paper's baselines / ablations */
@@ -454,7 +455,10 @@ int or_decide_batch(int M, int E, int nb, const int32_t *bs, const uint32_t *lat
 /* per-scenario statistics columns (same meaning as the library's, own enum) */
 enum {
   ST_DECISIONS = 0, ST_CANDIDATES, ST_CELLS, ST_COMPLETED, ST_VIOLATIONS,
-  ST_INFEASIBLE, ST_MAX_DEPTH, ST_STATUS, ST_SUM_LAT, ST_LIVE, ST_TERMS, ST_NCOL
+  ST_INFEASIBLE, ST_MAX_DEPTH, ST_STATUS, ST_SUM_LAT, ST_LIVE, ST_TERMS,
+  ST_ACC_BP, /* accuracy (basis points) of the served exit, summed over post-warmup tasks */
+  ST_EXIT0,  /* ST_EXIT0 + e: post-warmup tasks served at exit e (Fig. exit_depth) */
+  ST_NCOL = ST_EXIT0 + 8
 };
 
 static int cmp_u32(const void *a, const void *b) {
@@ -586,6 +590,10 @@ static int replay_one(const or_ctx *c, const uint64_t *n, const uint32_t *const 
         stats[ST_COMPLETED]++;
         stats[ST_SUM_LAT] += T;
         if (T > c->tau) stats[ST_VIOLATIONS]++; /* Eq. 2, strict (Q16) */
+        /* "for each completed task we record the exit point used,
+           look up the corresponding per-exit accuracy from Table I" */
+        if (c->acc) stats[ST_ACC_BP] += c->acc[best * c->E + d->e];
+        stats[ST_EXIT0 + d->e]++;
       }
       seq++;
     }
@@ -665,7 +673,7 @@ static void *replay_worker(void *arg) {
  * Scenarios are independent; nthreads > 1 only splits them over threads.
  */
 int or_replay_batch(int M, int E, int nb, const int32_t *bs, const uint32_t *lat,
-                    const uint8_t *mask, const uint32_t *tau, const uint32_t *C,
+                    const uint8_t *mask, const uint16_t *acc, const uint32_t *tau, const uint32_t *C,
                     const uint32_t *b_max, const uint32_t *warmup, const uint32_t *policy, int ncfg,
                     int64_t n_scen,
                     const uint16_t *cfg_idx, const uint64_t *arr_off, const uint32_t *arrival,
@@ -676,6 +684,7 @@ int or_replay_batch(int M, int E, int nb, const int32_t *bs, const uint32_t *lat
   or_ctx *ctx = (or_ctx *)calloc((size_t)ncfg, sizeof(or_ctx));
   for (int k = 0; k < ncfg; ++k) {
     int st = ctx_init(&ctx[k], M, E, nb, bs, lat, mask, tau[k], C[k], b_max[k], warmup[k], policy ? policy[k] : 0u);
+    ctx[k].acc = acc;
     if (st) {
       for (int q = 0; q < k; ++q) ctx_free(&ctx[q]);
       free(ctx);

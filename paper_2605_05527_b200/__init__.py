@@ -19,12 +19,13 @@ import numpy as np
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("ES_LIB") or os.path.join(_HERE, "libedgeserve.so")
 
-ES_NSTAT = 11
-ES_NGSTAT = 7
+ES_NSTAT = 20
+ES_NGSTAT = 16
 ES_HIST_BINS = 4096
 STAT_COLS = ["decisions", "candidates", "cells", "completed", "violations", "infeasible", "max_depth",
-             "status", "sum_lat", "live", "terms"]
-GROUP_COLS = ["decisions", "candidates", "cells", "completed", "violations", "infeasible", "sum_lat"]
+             "status", "sum_lat", "live", "terms", "acc_bp"] + [f"exit{e}" for e in range(8)]
+GROUP_COLS = ["decisions", "candidates", "cells", "completed", "violations", "infeasible", "sum_lat",
+              "acc_bp"] + [f"exit{e}" for e in range(8)]
 STATUS = {0: "ES_OK", 1: "ES_ERR_ARG", 2: "ES_ERR_PROFILE_GRID", 3: "ES_ERR_PROFILE_MONOTONE",
           4: "ES_ERR_OUT_OF_GRID", 5: "ES_ERR_RANGE", 6: "ES_ERR_CUDA", 7: "ES_ERR_OOM",
           8: "ES_ERR_UNSORTED", 9: "ES_ERR_NUMERIC", 10: "ES_ERR_INTERNAL"}
@@ -39,7 +40,7 @@ P = ctypes.c_void_p
 
 class ProfileDesc(ctypes.Structure):
     _fields_ = [("M", ctypes.c_int32), ("E", ctypes.c_int32), ("nb", ctypes.c_int32),
-                ("batch_sizes", P), ("latency_us", P), ("exit_mask", P)]
+                ("batch_sizes", P), ("latency_us", P), ("exit_mask", P), ("accuracy_bp", P)]
 
 
 class SchedCfg(ctypes.Structure):
@@ -163,8 +164,10 @@ def es_load_profile(profile, cfgs, device=0) -> Profile:
     bs = np.ascontiguousarray(profile.bs, np.int32)
     lat = np.ascontiguousarray(profile.lat, np.uint32)
     mask = None if profile.mask is None else np.ascontiguousarray(profile.mask, np.uint8)
+    acc = getattr(profile, "acc", None)
+    acc = None if acc is None else np.ascontiguousarray(acc, np.uint16)
     d = ProfileDesc(int(profile.M), int(profile.E), int(bs.size), bs.ctypes.data, lat.ctypes.data,
-                    None if mask is None else mask.ctypes.data)
+                    None if mask is None else mask.ctypes.data, None if acc is None else acc.ctypes.data)
     arr = (SchedCfg * len(cfgs))()
     for i, c in enumerate(cfgs):
         arr[i] = SchedCfg(int(c.tau), int(c.C), int(c.b_max), int(c.warmup), int(getattr(c, "policy", 0)))

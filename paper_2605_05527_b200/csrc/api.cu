@@ -95,6 +95,9 @@ es_status validate_profile(const es_profile_desc *d) {
     for (int e = 0; e < d->E; ++e) any |= d->exit_mask ? d->exit_mask[m * d->E + e] != 0 : true;
     if (!any) return fail(ES_ERR_PROFILE_GRID, "model %d has no allowed exit", m);
     for (int e = 0; e < d->E; ++e)
+      if (d->accuracy_bp && d->accuracy_bp[m * d->E + e] > 10000)
+        return fail(ES_ERR_ARG, "accuracy_bp(m=%d,e=%d)=%u above 10000 (100 %%)", m, e, d->accuracy_bp[m * d->E + e]);
+    for (int e = 0; e < d->E; ++e)
       for (int b = 0; b < d->nb; ++b) {
         const uint32_t v = d->latency_us[((size_t)m * d->E + e) * d->nb + b];
         if (v == 0u) return fail(ES_ERR_PROFILE_MONOTONE, "L(m=%d,e=%d,b=%d) = 0", m, e, b);
@@ -159,6 +162,8 @@ es_status es_load_profile(const es_profile_desc *desc, const es_sched_cfg *cfgs,
   off = align16(off + 2u * nb);
   lay.off_mask = off;
   off = align16(off + 4u * M);
+  lay.off_acc = off;
+  off = align16(off + 2u * M * E);
   lay.off_cfg = off;
   off = align16(off + (uint32_t)sizeof(CfgRec) * ncfg);
   std::vector<CfgRec> recs(ncfg);
@@ -218,6 +223,7 @@ es_status es_load_profile(const es_profile_desc *desc, const es_sched_cfg *cfgs,
       if (!desc->exit_mask || desc->exit_mask[m * E + e]) bits |= 1u << e;
     memcpy(img.data() + lay.off_mask + 4 * m, &bits, 4);
   }
+  if (desc->accuracy_bp) memcpy(img.data() + lay.off_acc, desc->accuracy_bp, 2u * M * E);
   memcpy(img.data() + lay.off_cfg, recs.data(), sizeof(CfgRec) * ncfg);
 
   {  // keep stream-ordered scratch (K1 streaming phases) cached in the pool

@@ -54,6 +54,7 @@ struct SmemProf {
   const uint32_t *lat;
   const uint16_t *bs;
   const uint32_t *mask;
+  const uint16_t *acc;  // [M][E] accuracy, basis points
   const CfgRec *cfg;
   int M, E, nb, ncfg;
 };
@@ -65,6 +66,7 @@ __device__ __forceinline__ SmemProf smem_prof(const uint8_t *sm, const ImgLayout
   p.lat = reinterpret_cast<const uint32_t *>(sm + lay.off_lat);
   p.bs = reinterpret_cast<const uint16_t *>(sm + lay.off_bs);
   p.mask = reinterpret_cast<const uint32_t *>(sm + lay.off_mask);
+  p.acc = reinterpret_cast<const uint16_t *>(sm + lay.off_acc);
   p.cfg = reinterpret_cast<const CfgRec *>(sm + lay.off_cfg);
   p.M = lay.M;
   p.E = lay.E;

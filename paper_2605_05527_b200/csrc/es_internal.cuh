@@ -6,6 +6,7 @@
 //   lat   u32 [M][E][nb]    L(m, e, bs[b]) in us
 //   bs    u16 [nb]          profiled batch sizes
 //   mask  u32 [M]           allowed-exit bitmask per model  (P:517-527 ablation)
+//   acc   u16 [M][E]        top-1 accuracy per (model, exit), basis points (Table I)
 //   cfg   CfgRec [ncfg]     per-SLO constants (tau, x_c, r, C_q, b_max, W, ...)
 //   per cfg c: A u32[nA_cap], Bt u32[1024], H u64[M*E*nb], bidx u8[b_max+1]
 // A, Bt, H, x_c, bidx are written on the GPU by k_build_tables (k_tables.cu).
@@ -38,7 +39,7 @@ struct ImgLayout {
   uint32_t bytes;       // total, multiple of 16
   uint32_t core_bytes;  // prefix without the per-cfg H tables (they form the tail)
   int32_t M, E, nb, ncfg;
-  uint32_t off_lat, off_bs, off_mask, off_cfg;
+  uint32_t off_lat, off_bs, off_mask, off_acc, off_cfg;
   // cfg 0's urgency-table constants (host-computed), kernel parameters for the
   // single-SLO specialisation of the K1 stream: byte offsets of A and Bt, 4 r,
   // and the A index mask 4 (2^k - 1) with 2^k >= nA_cap

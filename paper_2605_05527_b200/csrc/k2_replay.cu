@@ -97,6 +97,10 @@ __global__ void ES_K2_BOUNDS k2_replay(const uint8_t *__restrict__ gimg, ImgLayo
   // lane-local counters (reduced once per scenario)
   uint32_t completed = 0, viol = 0, cells = 0, maxd = 0;
   uint64_t sum_lat = 0, live_sum = 0, terms = 0;
+  // f1 statistics: the accuracy sum (lane 0 of the segment) and the exit-depth
+  // histogram, bin e held by segment lane e (LPS >= MAXE)
+  uint64_t acc_bp = 0;
+  uint32_t exit_n = 0;
 
   for (;;) {
     // ---- refill: segments without a scenario fetch the next one
@@ -142,6 +146,7 @@ __global__ void ES_K2_BOUNDS k2_replay(const uint8_t *__restrict__ gimg, ImgLayo
         decisions = candidates = infeasible = 0;
         completed = viol = cells = maxd = 0;
         sum_lat = live_sum = terms = 0;
+        acc_bp = exit_n = 0;
       }
     }
     if (__all_sync(FULL, exhausted)) break;
@@ -275,6 +280,12 @@ __global__ void ES_K2_BOUNDS k2_replay(const uint8_t *__restrict__ gimg, ImgLayo
           decisions++;
           candidates += ncand;
           if (!d.feas) infeasible++;
+          {  // f1: the batch's post-warmup tasks served at (m*, e*)
+            const uint32_t pre_w = seq < C.warmup ? min(C.warmup - seq, d.B) : 0u;
+            const uint32_t npost = d.B - pre_w;
+            if (sg.sl == 0) acc_bp += (uint64_t)npost * P.acc[d.m * P.E + d.e];
+            if ((uint32_t)sg.sl == d.e) exit_n += npost;
+          }
           if (sg.gl == 0 && len > 0u) {
             cells += nallow;
             live_sum += len - c;
@@ -331,8 +342,10 @@ __global__ void ES_K2_BOUNDS k2_replay(const uint8_t *__restrict__ gimg, ImgLayo
         st[ES_ST_SUM_LAT] = r_sum;
         st[ES_ST_LIVE] = r_live;
         st[ES_ST_TERMS] = r_terms;
+        st[ES_ST_ACC_BP] = acc_bp;
         if (status) report(a.dstat, status, s);
       }
+      if (sg.sl < MAXE) a.stats[s * ES_NSTAT + ES_ST_EXIT0 + sg.sl] = exit_n;
       active = false;
     }
   }

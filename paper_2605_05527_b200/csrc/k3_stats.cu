@@ -120,10 +120,12 @@ __global__ void __launch_bounds__(NT) k3_stats(StatsArgs a) {
     const uint32_t g = a.group_id ? a.group_id[s] : 0u;
     const bool grp = a.n_groups && g < a.n_groups;
     if (grp && threadIdx.x < ES_NGSTAT) {
-      const int col[ES_NGSTAT] = {ES_ST_DECISIONS, ES_ST_CANDIDATES, ES_ST_CELLS, ES_ST_COMPLETED,
-                                  ES_ST_VIOLATIONS, ES_ST_INFEASIBLE, ES_ST_SUM_LAT};
+      // group column -> scenario column: decisions .. infeasible, sum_lat, acc_bp, exit0 .. exit7
+      static_assert(ES_ST_INFEASIBLE == 5 && ES_ST_EXIT0 == ES_ST_ACC_BP + 1 && ES_ST_EXIT7 + 1 == ES_NSTAT, "cols");
+      const int t = (int)threadIdx.x;
+      const int col = t < 6 ? t : t == 6 ? ES_ST_SUM_LAT : ES_ST_ACC_BP + (t - 7);
       atomicAdd(reinterpret_cast<unsigned long long *>(a.counts + (uint64_t)g * ES_NGSTAT + threadIdx.x),
-                (unsigned long long)st[col[threadIdx.x]]);
+                (unsigned long long)st[col]);
     }
     const uint32_t W = a.cfg[k].warmup;
     const uint64_t base = a.arr_off[s * a.M];

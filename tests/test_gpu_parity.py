@@ -370,15 +370,15 @@ def test_group_merge_rank_count_invariance():
             shards.append((d, out))
         bufs = []
         for d, out in shards:
-            buf = torch.zeros(G * 7 + G * 4096, dtype=torch.uint64, device=DEV)
-            es.es_group_accumulate(h, d["arr_off"], d["arrival"], out, G, buf[:G * 7], buf[G * 7:], d["cfg_idx"],
+            buf = torch.zeros(G * es.ES_NGSTAT + G * 4096, dtype=torch.uint64, device=DEV)
+            es.es_group_accumulate(h, d["arr_off"], d["arrival"], out, G, buf[:G * es.ES_NGSTAT], buf[G * es.ES_NGSTAT:], d["cfg_idx"],
                                    d["group_id"])
             bufs.append(buf)
         tot = bufs[0].view(torch.int64).clone()
         for b in bufs[1:]:
             tot += b.view(torch.int64)
         tot = tot.view(torch.uint64)
-        counts, hist = tot[:G * 7], tot[G * 7:]
+        counts, hist = tot[:G * es.ES_NGSTAT], tot[G * es.ES_NGSTAT:]
         state = torch.zeros(2 * G, dtype=torch.uint64, device=DEV)
         es.es_group_p95_select(G, 0, counts, hist, state)
         for level in (1, 2):
@@ -389,7 +389,7 @@ def test_group_merge_rank_count_invariance():
                 acc += hl.view(torch.int64)
             es.es_group_p95_select(G, level, counts, acc.view(torch.uint64), state)
         torch.cuda.synchronize()
-        results.append((np_of(counts).reshape(G, 7), np_of(state).reshape(G, 2)[:, 0]))
+        results.append((np_of(counts).reshape(G, es.ES_NGSTAT), np_of(state).reshape(G, 2)[:, 0]))
     for c, p in results:
         assert np.array_equal(c, oc)
         assert np.array_equal(p.astype(np.uint32), op)
@@ -636,7 +636,7 @@ def test_k2_restricted_exit_masks(name, exits):
     keep = [0, E - 1] if exits == "layer1+final" else [2, E - 1]
     mask = np.zeros((w.profile.M, E), np.uint8)
     mask[:, keep] = 1
-    prof = inputs.Profile(w.profile.M, E, w.profile.bs, w.profile.lat, mask)
+    prof = inputs.Profile(w.profile.M, E, w.profile.bs, w.profile.lat, mask, w.profile.acc)
     w = inputs.Workload(w.name, prof, w.cfgs, w.traces, w.n_req)
     g = run_k2(w, dec_cap=1500)
     o = oracle.replay_batch(prof, w.cfgs, w.traces, dec_cap=1500, nthreads=8)
@@ -764,7 +764,7 @@ def test_full_size_cfg3_bench_config_sampled():
         assert np.array_equal(g["latency"][a:b], o["lat"][int(so[j * 8]):int(so[j * 8 + 8])]), s
     G = inputs.n_groups("cfg3")
     counts, p95 = es.group_merge(g["_handle"], g["_dev"], g["_out"], G, group=False)
-    cols = [0, 1, 2, 3, 4, 5, 8]
+    cols = oracle.GROUP_SRC
     ref = np.zeros((G, len(cols)), np.uint64)
     np.add.at(ref, w.traces.group_id.astype(np.int64), g["stats"][:, cols])
     assert np.array_equal(np_of(counts), ref)

@@ -60,6 +60,9 @@ def test_stat_columns_match_header():
     src = open(os.path.join(ROOT, "include", "edgeserve.h")).read()
     body = re.search(r"enum \{\s*ES_ST_DECISIONS = 0,(.*?)ES_NSTAT", src, re.S).group(0)
     cols = re.findall(r"ES_ST_(\w+)", body)
+    # the exit histogram is declared as the range ES_ST_EXIT0 .. ES_ST_EXIT7 = ES_ST_EXIT0 + 7
+    assert "ES_ST_EXIT7 = ES_ST_EXIT0 + 7" in body
+    cols = [c for c in cols if not c.startswith("EXIT")] + [f"EXIT{e}" for e in range(8)]
     assert len(cols) == es.ES_NSTAT == oracle.NCOL
     assert [c.lower() for c in cols] == es.STAT_COLS == oracle.COLS
 

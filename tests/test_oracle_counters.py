@@ -14,7 +14,7 @@ import oracle
 
 GOLD = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "work_counters.json")))
 COLS = ["decisions", "candidates", "cells", "completed", "violations", "infeasible", "max_depth", "status",
-        "sum_lat", "live", "terms"]
+        "sum_lat", "live", "terms", "acc_bp"]
 
 
 def golden_case(case):
@@ -22,7 +22,8 @@ def golden_case(case):
     p = GOLD[p] if isinstance(p, str) else p
     lat = np.asarray(p["lat"], np.uint32)
     prof = inputs.Profile(M=p["M"], E=p["E"], bs=np.asarray(p["bs"], np.int32), lat=lat,
-                          mask=np.ones((p["M"], p["E"]), np.uint8))
+                          mask=np.ones((p["M"], p["E"]), np.uint8),
+                          acc=np.asarray(p["acc"], np.uint16) if "acc" in p else None)
     c = case["cfg"]
     cfgs = [inputs.SchedCfg(tau=c["tau"], b_max=c["b_max"], C=c["C"], warmup=c["warmup"], policy=c["policy"])]
     segs = [[np.asarray(a, np.uint32) for a in case["arrivals"]]]
@@ -32,7 +33,8 @@ def golden_case(case):
 
 def expected_row(case):
     st = case["stats"]
-    return np.array([st.get(k, 0) for k in COLS], np.uint64)
+    ex = list(st["exit"]) + [0] * (8 - len(st["exit"]))
+    return np.array([st.get(k, 0) for k in COLS] + ex, np.uint64)
 
 
 @pytest.mark.parametrize("case", GOLD["cases"], ids=[c["name"][:40] for c in GOLD["cases"]])
