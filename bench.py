@@ -195,26 +195,11 @@ def k1_batch(rank, n_gen=4096, tiles=64, depth=4096):
     return q_off, w0, tiles
 
 
-def bench_k1(es, h_cache, dev, stream, rank, depth=4096, iters=10):
-    """K1 (es_score_candidates) on 5-C-shaped snapshots: M=8, E=5, batch 1-32,
-    per-model depth U[0, 4096], waits = t - Poisson arrivals in FIFO order.
-    Rates are set so a full queue spans ~120 ms < x_c - max L: every task is in
-    the live window and is read (the HBM-streaming regime).  262,144 snapshots
-    (17.3 GB of waits: SURVEY 5-C's full size; k1_batch).
-    Timed per launch with CUDA events, L2 flushed between launches."""
+def k1_time(es, h, dq, dw, dci, dev, stream, iters=10):
+    """Mean device time of one es_score_candidates call (CUDA events on the
+    launching stream, L2 flushed between launches) and the call's outputs."""
     import torch
-    import inputs
-    prof = inputs.synth_profile(8, 5, list(range(1, 33)))
-    cfgs = [inputs.SchedCfg(tau=50000, b_max=32)]
-    q_off, w0, tiles = k1_batch(rank, depth=depth)
-    n_snap = (q_off.size - 1) // 8
-    h = es.es_load_profile(prof, cfgs, device=dev.index)
-    tab = es.es_get_tables(h, 0)
-    n_live = int((w0 < tab["x_c"]).sum()) * tiles
-    dq = torch.from_numpy(q_off).to(dev)
-    dw = torch.from_numpy(w0).to(dev).repeat(tiles)
-    waits_size, waits_bytes = w0.size * tiles, w0.nbytes * tiles
-    out = es.es_score_candidates(h, dq, dw, stream=stream)
+    out = es.es_score_candidates(h, dq, dw, dci, stream=stream)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
     ms = []
     for i in range(iters + 2):
@@ -222,26 +207,110 @@ def bench_k1(es, h_cache, dev, stream, rank, depth=4096, iters=10):
         a = torch.cuda.Event(enable_timing=True)
         b = torch.cuda.Event(enable_timing=True)
         a.record(stream)
-        es.es_score_candidates(h, dq, dw, out=out, stream=stream)
+        es.es_score_candidates(h, dq, dw, dci, out=out, stream=stream)
         b.record(stream)
         torch.cuda.synchronize()
         if i >= 2:
             ms.append(a.elapsed_time(b))
-    t_s = statistics.mean(ms) / 1e3
-    M = 8
-    alg = n_snap * (8 * (M + 1) + 17 + 8 * M) + 4 * n_live
+    return statistics.mean(ms) / 1e3, out
+
+
+def k1_line(es, h, M, q_off, w0, tiles, ci, x_c, dev, stream, desc, kernel, traffic_key, iters=10):
+    """One K1 bench object: the distinct snapshots (q_off, w0, ci) repeated
+    `tiles` times back to back; algorithmic bytes = per snapshot the M+1 queue
+    offsets (8 B), the cfg index (2 B, when present) and the outputs (m, e, B,
+    L, S, flags and M candidate scores: 17 + 8 M B), plus 4 B per LIVE wait
+    (w < x_c of its cfg; the clipped prefix is counted from the index, never
+    read -- P:309 clip, Q24)."""
+    import torch
+    n0 = (q_off.size - 1) // M
+    nw = np.uint64(w0.size)
+    q = np.concatenate([q_off[:-1] + np.uint64(t) * nw for t in range(tiles)] + [q_off[-1:] + np.uint64(tiles - 1) * nw])
+    n_snap = n0 * tiles
+    dq = torch.from_numpy(q).to(dev)
+    dw = torch.from_numpy(w0).to(dev).repeat(tiles)
+    dci = None if ci is None else torch.from_numpy(np.tile(ci, tiles)).to(dev)
+    # live waits: per snapshot, waits below its cfg's x_c
+    if ci is None:
+        n_live = int((w0 < x_c[0]).sum()) * tiles
+    else:
+        snap_of_wait = np.repeat(np.arange(n0), np.diff(q_off[::M].astype(np.int64)))
+        n_live = int((w0 < np.asarray(x_c, np.uint64)[ci[snap_of_wait]]).sum()) * tiles
+    t_s, out = k1_time(es, h, dq, dw, dci, dev, stream, iters)
+    alg = n_snap * (8 * (M + 1) + (2 if ci is not None else 0) + 17 + 8 * M) + 4 * n_live
     hbm, _, src = peaks()
     flags = out["flags"].cpu().numpy()
-    return {"workload": f"5-C shape: {n_snap} snapshots x 8 DNNs x 5 exits x batch 1-32, depth U[0,{depth}] "
-                        f"per model, all tasks live ({waits_size} waits, {waits_bytes / 1e6:.0f} MB; "
-                        f"{n_snap // tiles} distinct seeded snapshots x {tiles})",
+    return {"workload": desc + f" ({n_snap} snapshots, {w0.size * tiles} waits of which {n_live} live, "
+                               f"{w0.nbytes * tiles / 1e6:.0f} MB; {n0} distinct x {tiles})",
             "snapshots_per_s": n_snap / t_s, "scored_candidates_per_s": float((out["cand"] != 0xFFFFFFFFFFFFFFFF)
                                                                              .sum().item()) / t_s,
             "ms_per_launch": t_s * 1e3, "feasible_frac": float((flags & 1).mean()),
             "roofline": {"bound": "hbm", "achieved": alg / t_s / 1e9, "peak": hbm, "unit": "GB/s",
-                         "frac": alg / t_s / 1e9 / hbm, "traffic": ncu_traffic("k1_call"),
-                         "kernel": "k1 call: k1s_prep + k1s_stream_tma + k1s_stream_slow + k1s_finish", "alg_bytes_per_launch": alg,
+                         "frac": alg / t_s / 1e9 / hbm, "traffic": ncu_traffic(traffic_key),
+                         "kernel": kernel, "alg_bytes_per_launch": alg,
                          "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({src})", "l2": "flushed between launches"}}
+
+
+def bench_k1(es, dev, stream, rank, depth=4096):
+    """K1 (es_score_candidates) on 5-C-shaped snapshots: M=8, E=5, batch 1-32,
+    per-model depth U[0, 4096], waits = t - Poisson arrivals in FIFO order.
+    Rates are set so a full queue spans ~120 ms < x_c - max L: every task is in
+    the live window and is read (the HBM-streaming regime).  262,144 snapshots
+    (17.3 GB of waits: SURVEY 5-C's full size; k1_batch)."""
+    import inputs
+    prof = inputs.synth_profile(8, 5, list(range(1, 33)))
+    cfgs = [inputs.SchedCfg(tau=50000, b_max=32)]
+    q_off, w0, tiles = k1_batch(rank, depth=depth)
+    h = es.es_load_profile(prof, cfgs, device=dev.index)
+    x_c = [es.es_get_tables(h, 0)["x_c"]]
+    n0 = (q_off.size - 1) // 8 // tiles
+    return k1_line(es, h, 8, q_off[:n0 * 8 + 1], w0, tiles, None, x_c, dev, stream,
+                   f"5-C shape: 8 DNNs x 5 exits x batch 1-32, depth U[0,{depth}] per model, all tasks live",
+                   "k1 call: k1s_prep + k1s_stream_tma + k1s_stream_slow + k1s_finish", "k1_call")
+
+
+def bench_k1_clip(es, dev, stream, rank, depth=4096):
+    """K1 on 5-C depth under 5-B's overload rates (rates_for_shallow_load,
+    rho 1.5): queue heads wait past x_c - max L, so every snapshot takes the
+    general per-candidate clip path and long clipped prefixes are
+    counted, not read."""
+    import inputs
+    prof = inputs.synth_profile(8, 5, list(range(1, 33)))
+    cfgs = [inputs.SchedCfg(tau=50000, b_max=32)]
+    rate = inputs.rates_for_shallow_load(prof, 32, 1.5)
+    q_off, w0 = inputs.snapshots_poisson_depth(2000 + rank, np.arange(4096), 8, depth, rate)
+    h = es.es_load_profile(prof, cfgs, device=dev.index)
+    x_c = [es.es_get_tables(h, 0)["x_c"]]
+    return k1_line(es, h, 8, q_off, w0, 64, None, x_c, dev, stream,
+                   f"5-C depth U[0,{depth}] at 5-B overload rates (rho_shallow 1.5): heads past x_c - max L, "
+                   "the general clip path", "k1 call (clip path)", "k1_clip")
+
+
+def bench_k1_harvested(es, engine, dev, stream, rank, n_scen=512, tiles=8):
+    """K1 on queue snapshots harvested at the decision instants of cfg3
+    replays ('harvested config-3 snapshots'): n_scen cfg3
+    scenarios replayed by K2 with the decision log on, every decision's queue
+    state rebuilt on the host (inputs.harvest_snapshots, pure indexing), nine
+    SLO configs mixed by the snapshots' cfg index -- the warp-segment mapping."""
+    import torch
+    import inputs
+    w = inputs.workload("cfg3", scen_ids=np.arange(rank * n_scen, (rank + 1) * n_scen))
+    h = es.es_load_profile(w.profile, w.cfgs, device=dev.index)
+    d = engine.upload_traces(w.traces, dev)
+    cap = int(max(np.diff(w.traces.arr_off.astype(np.int64)[::w.profile.M])))  # <= one decision per request
+    o = es.es_replay_traces(h, d["arr_off"], d["arrival"], d["cfg_idx"], d["group_id"], full=True, p95=False,
+                            dec_cap=cap, stream=stream)
+    torch.cuda.synchronize()
+    n_dec = o["stats"][:, 0].cpu().numpy()
+    q_off, w0, ci = inputs.harvest_snapshots(w.traces, n_dec, cap, o["dec_t"].cpu().numpy(),
+                                             o["dec_m"].cpu().numpy(), o["dec_B"].cpu().numpy())
+    del o, d
+    x_c = [es.es_get_tables(h, k)["x_c"] for k in range(len(w.cfgs))]
+    live_per = float(np.mean(np.diff(q_off[::8].astype(np.int64))))
+    return k1_line(es, h, 8, q_off, w0, tiles, ci, x_c, dev, stream,
+                   f"cfg3 harvested: every decision instant of {n_scen} cfg3 scenarios (8 DNNs x 5 exits x batch "
+                   f"1-32, 9 SLOs), {live_per:.1f} queued tasks per snapshot on average",
+                   "k1 call (warp-segment mapping)", "k1_harvested")
 
 
 def run_reference(args, rank, world):
@@ -504,7 +573,9 @@ def main():
 
     # ---------------- K1: independent snapshot scoring, the HBM-streaming form
     if not args.no_k1 and not args.ncu:
-        line["k1"] = bench_k1(es, h_cache={}, dev=dev, stream=stream, rank=rank)
+        line["k1"] = bench_k1(es, dev, stream, rank)
+        line["k1_clip"] = bench_k1_clip(es, dev, stream, rank)
+        line["k1_harvested"] = bench_k1_harvested(es, engine, dev, stream, rank)
 
     # ---------------- the other configs' headline lines (K2 + K3 + merge per step)
     if args.workload == "cfg3" and not args.no_extra and not args.ncu:

@@ -317,6 +317,59 @@ def snapshots_poisson_depth(seed, scen_ids, M, depth_max, rate_per_us):
     return q_off, waits
 
 
+def harvest_snapshots(traces, n_dec, dec_cap, dec_t, dec_m, dec_B, max_snap=None):
+    """Queue snapshots at the decision instants of a replay log (any
+    scheduler's: the caller passes its per-scenario decision times, chosen
+    models and batch sizes, log stride dec_cap).  Snapshot k of scenario s
+    holds, per model m, the waits t_k - a of the requests of Q_m that arrived
+    by t_k (a <= t_k, reading Q10) and were not yet dispatched (the dispatched
+    ones are the first sum of B over earlier decisions on m).  Pure indexing,
+    no scheduling arithmetic.  Returns (q_off u64 [n*M+1], waits u32, cfg_idx
+    u16 [n]) in scenario-major, decision order."""
+    M = traces.M
+    q_lens, parts, ci = [], [], []
+    taken = 0
+    for s in range(traces.n_scen):
+        k = int(n_dec[s])
+        if max_snap is not None:
+            k = min(k, max_snap - taken)
+        if k <= 0:
+            break
+        t = dec_t[s * dec_cap:s * dec_cap + k].astype(np.int64)
+        dm = dec_m[s * dec_cap:s * dec_cap + k].astype(np.int64)
+        dB = dec_B[s * dec_cap:s * dec_cap + k].astype(np.int64)
+        lens = np.zeros((k, M), np.int64)
+        per_m = []
+        for m in range(M):
+            arr = traces.arrival[int(traces.arr_off[s * M + m]):int(traces.arr_off[s * M + m + 1])].astype(np.int64)
+            tail = np.searchsorted(arr, t, side="right")
+            served = np.where(dm == m, dB, 0)
+            head = np.cumsum(served) - served  # dispatched before decision k
+            ln = np.maximum(tail - head, 0)
+            lens[:, m] = ln
+            # flat gather: for each snapshot, arr[head:head+ln]
+            tot = int(ln.sum())
+            start = np.repeat(head - (np.cumsum(ln) - ln), ln)
+            idx = np.arange(tot, dtype=np.int64) + start
+            per_m.append((ln, t.repeat(ln) - arr[idx]))
+        # interleave: snapshot-major, model-minor
+        seg_len = lens.reshape(-1)
+        out = np.empty(int(seg_len.sum()), np.uint32)
+        dst_off = np.concatenate([[0], np.cumsum(seg_len)[:-1]]).reshape(k, M)
+        for m in range(M):
+            ln, w = per_m[m]
+            dst = np.repeat(dst_off[:, m] - (np.cumsum(ln) - ln), ln) + np.arange(int(ln.sum()), dtype=np.int64)
+            out[dst] = w
+        q_lens.append(seg_len)
+        parts.append(out)
+        ci.append(np.full(k, int(traces.cfg_idx[s]), np.uint16))
+        taken += k
+    seg = np.concatenate(q_lens).astype(np.uint64)
+    q_off = np.zeros(seg.size + 1, np.uint64)
+    np.cumsum(seg, out=q_off[1:])
+    return q_off, np.concatenate(parts), np.concatenate(ci)
+
+
 # --------------------------------------------------------------------------- workloads
 
 

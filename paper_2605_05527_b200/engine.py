@@ -42,7 +42,7 @@ def group_merge(prof, dtr, out, n_groups, group=None, stream=None, with_p95=Fals
     outputs.  group: a torch.distributed process group (None = default when
     initialised, False = local only).  with_p95: also compute the per-scenario
     P95 (K3) in the same pass as the level-0 histogram.  Returns
-    (counts u64 [G][7], p95 u64 [G]).
+    (counts u64 [G][ES_NGSTAT], p95 u64 [G]).
     """
     import torch
     from . import ES_HIST_BINS, ES_NGSTAT, es_group_hist, es_group_p95_select, es_scen_stats

@@ -171,23 +171,7 @@ def test_k1_harvested_snapshots():
         M = w.profile.M
         cap = 3000
         o = oracle.replay_batch(w.profile, w.cfgs, w.traces, dec_cap=cap)
-        q_off = [0]
-        ws = []
-        ci = []
-        for s in range(len(ids)):
-            arr = w.traces.scenario(s)
-            head = [0] * M
-            for k in range(int(o["stats"][s, 0])):
-                t = int(o["dec_t"][s * cap + k])
-                for m in range(M):
-                    tail = int(np.searchsorted(arr[m], t, side="right"))
-                    ws.extend(t - int(a) for a in arr[m][head[m]:tail])
-                    q_off.append(len(ws))
-                ci.append(int(w.traces.cfg_idx[s]))
-                head[int(o["dec_m"][s * cap + k])] += int(o["dec_B"][s * cap + k])
-        q_off = np.array(q_off, np.uint64)
-        ws = np.array(ws, np.uint32)
-        ci = np.array(ci, np.uint16)
+        q_off, ws, ci = inputs.harvest_snapshots(w.traces, o["stats"][:, 0], cap, o["dec_t"], o["dec_m"], o["dec_B"])
         g = run_k1(w.profile, w.cfgs, q_off, ws, ci)
         r = oracle.decide_batch(w.profile, w.cfgs, q_off, ws, ci)
         assert_k1_equal(g, r, M)
