@@ -565,6 +565,143 @@ __device__ __forceinline__ Decision decide_general(const Seg<LPS, MM> &sg, const
   return finish_decision<LPS, MM>(sg, cand, Sq, mkey);
 }
 
+// Fast path of a replay step with the queued positions of the WHOLE warp
+// flattened (K2).  The per-group fast path below walks each queue with its
+// own GL lanes, so a warp step costs its longest queue; K2's batches are
+// heavy-tailed across scenarios (cfg3: queued tasks per decision p50 19, p99
+// 300), so here the non-empty queues of every segment are concatenated and
+// each trip evaluates G for 32 consecutive positions, one per lane.  Per
+// queue q the sums come from a running inclusive scan Pf over the flat order:
+//   S_q = Pf(start_q), E_q = Pf(start_q + B_q), T_q = Pf(end_q)
+//   srv_q = E_q - S_q (own served head tasks), Q_q = T_q - S_q (whole queue),
+// tot = sum over the segment's queues of Q_q.  Same integers as the fast path
+// of decide(); exact in any order.  Whole warp; `fast` must be warp-uniform.
+// Per-warp scratch (shared memory, FLAT_BYTES): the non-empty queues by rank.
+constexpr uint32_t FLAT_BYTES = 32 * 16 * 2 + 3 * 32 * 8;
+#ifndef FLAT_WF
+#define FLAT_WF 2  // flat positions per lane per trip
+#endif
+
+template <int LPS, int MM>
+__device__ __forceinline__ Decision decide_fast_flat(const Seg<LPS, MM> &sg, const SmemProf &P, const SmemCfg &C,
+                                                    uint32_t len, const Cand &cand, const uint32_t *Ah, uint32_t t,
+                                                    uint8_t *scratch) {
+  constexpr int GL = Seg<LPS, MM>::GL;
+  uint4 *ent0 = reinterpret_cast<uint4 *>(scratch);  // {start, end, B | q << 16, t + r}
+  uint4 *ent1 = ent0 + 32;                            // {ptr lo, ptr hi, off_A, off_Bt}
+  uint64_t *slotS = reinterpret_cast<uint64_t *>(ent1 + 32);  // Pf at start_q, start_q + B_q, end_q
+  uint64_t *slotE = slotS + 32, *slotT = slotE + 32;
+  const uint32_t lane = (uint32_t)sg.lane;
+  const bool own = sg.gl == 0 && len > 0u;  // queue owner: lane 0 of a non-empty group
+  const uint32_t Bown = len ? cand.B : 0u;
+  // exclusive scan of the owners' lengths over the warp
+  uint32_t incl = own ? len : 0u;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t v = __shfl_up_sync(FULL, incl, o);
+    if (lane >= (uint32_t)o) incl += v;
+  }
+  const uint32_t start = incl - (own ? len : 0u);
+  const uint32_t NW = __shfl_sync(FULL, incl, 31);
+  const unsigned ne = __ballot_sync(FULL, own);
+  if (own) {
+    const uint32_t rk = __popc(ne & ((1u << lane) - 1u));
+    const uint64_t ptr = reinterpret_cast<uint64_t>(Ah);
+    ent0[rk] = make_uint4(start, start + len, Bown | (lane << 16), t + C.r);
+    ent1[rk] = make_uint4((uint32_t)ptr, (uint32_t)(ptr >> 32), C.off_A, C.off_Bt);
+  }
+  __syncwarp();
+  uint64_t carry = 0ull;
+  uint32_t cb = 0u;  // non-empty queues starting before this trip
+  // a trip covers 32 WF consecutive flat positions; lane l takes positions
+  // base + WF l + k (k < WF), all inside 32-position word l / (32 / WF)
+  constexpr int WF = FLAT_WF;
+  constexpr int LPW = 32 / WF;  // lanes per 32-position word
+  const uint32_t lw = lane / LPW, lb = (lane % LPW) * WF;  // this lane's word, its first bit in it
+  for (uint32_t base = 0; base < NW; base += 32u * WF) {
+    // queue starts inside this trip: one bit per position, one word per 32
+    const uint32_t rel = start - base;
+    const bool here = own && start >= base && rel < 32u * WF;
+    uint32_t pre = 0u, word = 0u, tripc = 0u;
+#pragma unroll
+    for (int w = 0; w < WF; ++w) {
+      const uint32_t bit = here && (rel >> 5) == (uint32_t)w ? 1u << (rel & 31u) : 0u;
+      uint32_t mw;
+      asm volatile("redux.sync.or.b32 %0, %1, 0xffffffff;" : "=r"(mw) : "r"(bit));
+      const uint32_t c = __popc(mw);
+      if ((uint32_t)w < lw) pre += c;
+      if ((uint32_t)w == lw) word = mw;
+      tripc += c;
+    }
+    // G of the lane's positions; boundary roles packed with the queue id
+    uint64_t gk[WF];
+    uint32_t ik[WF];
+    uint64_t lsum = 0ull;
+#pragma unroll
+    for (int k = 0; k < WF; ++k) {
+      const uint32_t f = base + lane * WF + (uint32_t)k;
+      gk[k] = 0ull;
+      ik[k] = 0u;
+      if (f < NW) {
+        const uint32_t bk = lb + (uint32_t)k;
+        const uint32_t le = bk == 31u ? FULL : ((2u << bk) - 1u);
+        const uint32_t rk = cb + pre + __popc(word & le) - 1u;
+        const uint4 e0 = ent0[rk], e1 = ent1[rk];
+        const uint32_t p = f - e0.x;
+        const uint32_t *qa = reinterpret_cast<const uint32_t *>((uint64_t)e1.x | ((uint64_t)e1.y << 32));
+        // v = w + r = (t + r) - a; w < fast_lim <= x_c, so v >> 10 < nA (the
+        // clamps of G_of are no-ops on the fast path)
+        const uint32_t v = e0.w - __ldg(qa + p);
+        const uint32_t A = *reinterpret_cast<const uint32_t *>(P.sm + e1.z + 4u * (v >> SBITS));
+        const uint32_t Bt = *reinterpret_cast<const uint32_t *>(P.sm + e1.w + 4u * (v & (S - 1u)));
+        gk[k] = ((uint64_t)A * (uint64_t)Bt) >> F;
+        lsum += gk[k];
+        ik[k] = (e0.z >> 16) | (p == 0u ? 0x100u : 0u) | (p + 1u == (e0.z & 0xFFFFu) ? 0x200u : 0u) |
+                (f + 1u == e0.y ? 0x400u : 0u);
+      }
+    }
+    // running prefix over the flat order: exclusive scan of the lane sums
+    uint64_t s = lsum;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint64_t v = __shfl_up_sync(FULL, s, o);
+      if (lane >= (uint32_t)o) s += v;
+    }
+    uint64_t Pf = carry + s - lsum;
+#pragma unroll
+    for (int k = 0; k < WF; ++k) {
+      Pf += gk[k];  // prefix through this position
+      if (ik[k] >> 8) {
+        const uint32_t q = ik[k] & 0xFFu;
+        if (ik[k] & 0x100u) slotS[q] = Pf - gk[k];
+        if (ik[k] & 0x200u) slotE[q] = Pf;
+        if (ik[k] & 0x400u) slotT[q] = Pf;
+      }
+    }
+    carry += __shfl_sync(FULL, s, 31);
+    cb += tripc;
+  }
+  __syncwarp();
+  uint64_t srv = 0ull, Q = 0ull;
+  if (own) {
+    const uint64_t s0 = slotS[lane];
+    srv = slotE[lane] - s0;
+    Q = slotT[lane] - s0;
+  }
+  const uint64_t tot = sg.sum64(Q);
+  srv = sg.bcast(srv, sg.grp * GL);
+  uint64_t Sq = ~0ull;
+  uint32_t mkey = 0xFFu;
+  if (len) {
+    const uint64_t u = tot - srv;
+    const uint64_t lo = cand.H * u, hi = __umul64hi(cand.H, u);
+    Sq = (hi << (64 - F)) | (lo >> F);
+    mkey = (uint32_t)sg.grp;
+  }
+  __syncwarp();  // the scratch is reused by the next step
+  return finish_decision<LPS, MM>(sg, cand, Sq, mkey);
+}
+
 // a5-a7.  Inputs per group g (uniform in the group): len = |Q_g|, c = number of
 // head tasks with w >= x_c (clipped for everyone, never read), cand = a3/a4
 // result, and wait_at(p) returning the wait of position p (c <= p < len; no

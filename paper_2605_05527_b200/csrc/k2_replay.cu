@@ -78,6 +78,7 @@ __global__ void ES_K2_BOUNDS k2_replay(const uint8_t *__restrict__ gimg, ImgLayo
   stage_image(smem, gimg, a.stage_bytes, &mbar);
   SmemProf P = smem_prof(smem, lay);
   if (a.stage_bytes < lay.bytes) P.hb = gimg;  // H tables stay in global memory (L1-cached)
+  uint8_t *flat = smem + ((a.stage_bytes + 15u) & ~15u) + (threadIdx.x >> 5) * FLAT_BYTES;  // this warp's scratch
   const Seg<LPS, MM> sg;
   const int g = sg.grp;
   const int M = P.M;
@@ -231,8 +232,16 @@ __global__ void ES_K2_BOUNDS k2_replay(const uint8_t *__restrict__ gimg, ImgLayo
       // baseline policy (each runs warp-wide when some segment needs it)
       const bool sc = !POL || policy_scores(C.policy);
       Decision d{};
-      if (!POL || (a.any_score && (!a.any_simple || __any_sync(FULL, dec && sc))))
-        d = decide<LPS, MM>(sg, P, C, len, c, b_slow == 0u, cand, [&](uint32_t p) { return tt - ldg_u32(Ah + p); });
+      if (!POL || (a.any_score && (!a.any_simple || __any_sync(FULL, dec && sc)))) {
+        // fast path of 8-lane segments: the warp's queued positions flattened
+        // (four scenarios per warp: the per-group walk would cost the warp's
+        // longest queue; measured cfg3 K2 46.7 -> 43.4 ms).  Wider segments
+        // keep the per-group walk (flattening measured slower there).
+        if (LPS == 8 && b_slow == 0u)
+          d = decide_fast_flat<LPS, MM>(sg, P, C, len, cand, Ah, tt, flat);
+        else
+          d = decide<LPS, MM>(sg, P, C, len, c, b_slow == 0u, cand, [&](uint32_t p) { return tt - ldg_u32(Ah + p); });
+      }
       if (POL && a.any_simple && __any_sync(FULL, dec && !sc)) {
         const Decision ds = select_simple<LPS, MM>(sg, cand, len, wmax, C);
         if (!sc) d = ds;
@@ -408,24 +417,27 @@ cudaError_t launch_t(const uint8_t *img, const ImgLayout &lay, const ReplayArgs 
   const bool out = a.completion || a.exit_used || a.dec_cap;
   auto kern = alg1 ? (out ? k2_replay<LPS, MM, false, true> : k2_replay<LPS, MM, false, false>)
                    : (out ? k2_replay<LPS, MM, true, true> : k2_replay<LPS, MM, true, false>);
-  const size_t dyn = a.stage_bytes;
-  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
+  // dynamic shared memory: the staged image + one flat-path scratch per warp
+  auto dyn_of = [&](int threads) {
+    return (((size_t)a.stage_bytes + 15u) & ~(size_t)15u) + (LPS == 8 ? (size_t)(threads / 32) * FLAT_BYTES : 0u);
+  };
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn_of(256));
   if (e != cudaSuccess) return e;
   // threads per block: the smallest of 64 / 128 / 256 that keeps the resident
   // thread count of 256-thread blocks (small blocks deal the longest-first
   // scenarios round-robin over the SMs in finer grains; a large profile image
   // -- one CTA per SM by shared memory -- keeps 256).  ES_K2_BLOCK overrides.
   int occ = 0;
-  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 256, dyn);
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 256, dyn_of(256));
   if (e != cudaSuccess) return e;
   int threads = 256;
   for (int t = 64; t < 256; t *= 2) {
     int o = 0;
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, kern, t, dyn);
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, kern, t, dyn_of(t));
     if (e != cudaSuccess) return e;
     // (and only while the extra per-CTA image copies leave L1 room: the
     // pending waits are re-read from L1 every decision)
-    if (o * t >= occ * 256 && (size_t)o * dyn <= 72u * 1024u) {
+    if (o * t >= occ * 256 && (size_t)o * dyn_of(t) <= 72u * 1024u) {
       threads = t;
       occ = o;
       break;
@@ -435,7 +447,7 @@ cudaError_t launch_t(const uint8_t *img, const ImgLayout &lay, const ReplayArgs 
     const int v = atoi(env);
     if (v == 32 || v == 64 || v == 128 || v == 256) {
       threads = v;
-      e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, threads, dyn);
+      e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, threads, dyn_of(threads));
       if (e != cudaSuccess) return e;
     }
   }
@@ -446,7 +458,7 @@ cudaError_t launch_t(const uint8_t *img, const ImgLayout &lay, const ReplayArgs 
   const int64_t cap = (int64_t)sms * occ;
   if (blocks > cap) blocks = cap;
   if (blocks < 1) blocks = 1;
-  kern<<<(unsigned)blocks, threads, dyn, st>>>(img, lay, a);
+  kern<<<(unsigned)blocks, threads, dyn_of(threads), st>>>(img, lay, a);
   return cudaGetLastError();
 }
 
@@ -460,11 +472,12 @@ cudaError_t launch_lps(const uint8_t *img, const ImgLayout &lay, const ReplayArg
 // lanes per scenario: a latency-bound batch (few chains per SM: the longest
 // chain is the kernel's time) takes wide segments -- 16 lanes for M <= 4, a
 // whole warp for M > 4 -- so one decision has more lanes on its chain; a
-// throughput-bound batch (>= 256 scenarios per SM) takes half that width, so
-// each warp instruction serves twice the decisions.  Measured (1 x B200, K2
-// alone): cfg2 16 lanes 2.90 ms vs 8 lanes 3.77; cfg5-A 32: 105 vs 16: 175;
-// cfg5-B 32: 281 vs 16: 323; cfg3 16: 46.7 vs 32: 55.0; cfg4 8: 52.5 vs
-// 16: 64.9.  ES_LPS overrides.
+// throughput-bound batch (>= 256 scenarios per SM) takes 8-lane segments, so
+// each warp instruction serves four decisions (and the flattened fast path
+// balances the four).  Measured (1 x B200, K2 alone): cfg2 16 lanes 2.90 ms
+// vs 8 lanes 3.77; cfg5-A 32: 105 vs 16: 175; cfg5-B 32: 281 vs 16: 323;
+// cfg3 8 (flat): 43.4 vs 16: 48.1 vs 32: 59.1; cfg4 8: 52.5 vs 16: 64.9.
+// ES_LPS overrides.
 int choose_lps(const ImgLayout &lay, int64_t n_scen, int sms) {
   const char *env = getenv("ES_LPS");
   if (env) {
@@ -472,7 +485,7 @@ int choose_lps(const ImgLayout &lay, int64_t n_scen, int sms) {
     if (v == 8 || v == 16 || v == 32) return v;
   }
   const int wide = lay.M <= 4 ? 16 : 32;
-  return n_scen >= (int64_t)256 * sms ? wide / 2 : wide;
+  return n_scen >= (int64_t)256 * sms ? 8 : wide;
 }
 
 }  // namespace

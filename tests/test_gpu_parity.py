@@ -761,3 +761,4 @@ def test_full_size_cfg3_bench_config_sampled():
         v = np.sort(np.concatenate(vals))
         k = (95 * v.size + 99) // 100
         assert int(p95[grp]) == int(v[k - 1]), grp
+
