@@ -293,22 +293,23 @@ __device__ __forceinline__ Cand cand_params(const Seg<LPS, MM> &sg, const SmemPr
     if (k.L >= C.x_c) k.H = 0ull;
     return k;
   }
-  // more exits than group lanes: every lane evaluates Eq. 6 for all exits of
-  // its group's model itself (E independent shared-memory loads, no ballot
-  // rounds on the decision's chain)
-  uint32_t Lv[MAXE];
-#pragma unroll
-  for (int e = 0; e < MAXE; ++e) Lv[e] = e < P.E ? row[e * P.nb] : 0xFFFFFFFFu;
-#pragma unroll
-  for (int e = 0; e < MAXE; ++e)
-    if (e < P.E && ((mbits >> e) & 1u) && (uint64_t)wmax + Lv[e] <= (uint64_t)C.tau) bits |= 1u << e;
+  // more exits than group lanes: every lane evaluates Eq. 6 for its group's
+  // model itself.  L is strictly increasing in e (validated), so the exits
+  // with wmax + L <= tau are the first c ones: c by a 4-step binary search
+  // (E <= 8), then the mask keeps the allowed ones.
+  if (wmax <= C.tau) {
+    const uint32_t lim = C.tau - wmax;  // wmax + L <= tau  <=>  L <= lim
+    uint32_t c = 0u;  // binary lifting: c < 16 covers E <= 8
+    if (8 <= P.E && row[7 * P.nb] <= lim) c = 8u;
+    if (c + 4u <= (uint32_t)P.E && row[(c + 3u) * P.nb] <= lim) c += 4u;
+    if (c + 2u <= (uint32_t)P.E && row[(c + 1u) * P.nb] <= lim) c += 2u;
+    if (c + 1u <= (uint32_t)P.E && row[c * P.nb] <= lim) c += 1u;
+    bits = ((1u << c) - 1u) & mbits;
+  }
   k.feas = bits != 0u;
   k.e = k.feas ? 31u - __clz(bits) : (uint32_t)(__ffs(mbits) - 1);
   if (fixed) k.e = fixed == 1 ? 31u - __clz(mbits) : (uint32_t)(__ffs(mbits) - 1);
-  k.L = Lv[0];
-#pragma unroll
-  for (int e = 1; e < MAXE; ++e)
-    if ((uint32_t)e == k.e) k.L = Lv[e];
+  k.L = row[k.e * P.nb];
   if (fixed) k.feas = (uint64_t)wmax + k.L <= (uint64_t)C.tau;
   k.thr = k.L < C.x_c ? C.x_c - k.L : 0u;
   k.H = k.L < C.x_c ? reinterpret_cast<const uint64_t *>(P.hb + C.off_H)[((size_t)gg * P.E + k.e) * P.nb + bi]

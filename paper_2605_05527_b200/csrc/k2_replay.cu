@@ -92,7 +92,17 @@ __global__ void ES_K2_BOUNDS k2_replay(const uint8_t *__restrict__ gimg, ImgLayo
   uint64_t base0 = 0, qb = 0;
   const uint32_t *Aq = a.arrival;
   uint32_t n = 0, head = 0, tail = 0, live = 0, last = 0, next_arr = 0xFFFFFFFFu;
-  uint32_t win = 0xFFFFFFFFu;  // arrival at position tail + gl (admission window, loaded ahead)
+  // admission window: WA consecutive arrivals per lane, a GW-arrival window
+  // per group per round (narrow groups take several per lane: bursts admit in
+  // fewer rounds), loaded one decision ahead
+#ifndef ES_K2_WIN
+#define ES_K2_WIN 4
+#endif
+  constexpr int WA = GL >= ES_K2_WIN ? 1 : ES_K2_WIN / GL;
+  constexpr int GW = GL * WA;
+  uint32_t win[WA];
+#pragma unroll
+  for (int k = 0; k < WA; ++k) win[k] = 0xFFFFFFFFu;
   uint32_t t = 0, total = 0, served = 0, seq = 0, status = 0, iters = 0;
   uint64_t decisions = 0, candidates = 0, infeasible = 0;
   // lane-local counters (reduced once per scenario)
@@ -131,7 +141,11 @@ __global__ void ES_K2_BOUNDS k2_replay(const uint8_t *__restrict__ gimg, ImgLayo
         }
         Aq = a.arrival + qb;
         if (n_new) a0 = ldg_u32(Aq);
-        win = (uint32_t)sg.gl < n_new ? ldg_u32(Aq + sg.gl) : 0xFFFFFFFFu;
+#pragma unroll
+        for (int k = 0; k < WA; ++k) {
+          const uint32_t i = (uint32_t)(sg.gl * WA + k);
+          win[k] = i < n_new ? ldg_u32(Aq + i) : 0xFFFFFFFFu;
+        }
       }
       const uint32_t tot = sg.sum(sg.gl == 0 ? n_new : 0u);
       const uint32_t t0 = sg.vmin(a0);
@@ -163,30 +177,57 @@ __global__ void ES_K2_BOUNDS k2_replay(const uint8_t *__restrict__ gimg, ImgLayo
       const uint32_t ahead_pre = pre_ok ? ldg_u32(Aq + head) : 0u;  // head arrival, issued early
       bool more = true, first = true;
       while (more) {
-        const uint32_t idx = tail + sg.gl;
-        const bool valid = run && idx < n;
-        // first round: the register window loaded at the end of the previous
-        // admission (its load is off this decision's chain)
-        const uint32_t v = !valid ? 0xFFFFFFFFu : first ? win : ldg_u32(Aq + idx);
+        // window positions tail + gl WA + k; the first round reads the
+        // registers loaded at the end of the previous admission (off the chain)
+        uint32_t v[WA];
+        uint32_t c = 0u;
+        bool bad = false;
+#pragma unroll
+        for (int k = 0; k < WA; ++k) {
+          const uint32_t idx = tail + (uint32_t)(sg.gl * WA + k);
+          const bool valid = run && idx < n;
+          v[k] = !valid ? 0xFFFFFFFFu : first ? win[k] : ldg_u32(Aq + idx);
+          c += valid && v[k] <= t ? 1u : 0u;
+          if (k > 0) bad |= valid && v[k] < v[k - 1];
+        }
         first = false;
-        uint32_t prev = __shfl_up_sync(FULL, v, 1, GL);
-        if (sg.gl == 0) prev = last;
-        const bool ok = valid && v <= t;
-        const unsigned bal = __ballot_sync(FULL, ok);
-        const unsigned badb = __ballot_sync(FULL, valid && v < prev);
-        const uint32_t cnt = __popc(sg.gbits(bal));
-        const uint32_t lv = __shfl_sync(FULL, v, sg.grp * GL + (cnt ? cnt - 1 : 0), LPS);
-        const uint32_t nx = __shfl_sync(FULL, v, sg.grp * GL + (cnt < GL ? cnt : GL - 1), LPS);
+        uint32_t prev = last;  // order check across lanes: the previous lane's last element
+        if constexpr (GL > 1) {
+          const uint32_t pl = __shfl_up_sync(FULL, v[WA - 1], 1, GL);
+          if (sg.gl != 0) prev = pl;
+        }
+        bad |= run && tail + (uint32_t)(sg.gl * WA) < n && v[0] < prev;
+        // admitted = a prefix of the group window (sorted): its length
+        uint32_t cnt = c;
+#pragma unroll
+        for (int o = 1; o < GL; o <<= 1) cnt += __shfl_xor_sync(FULL, cnt, o, GL);
+        const unsigned badb = __ballot_sync(FULL, bad);
+        // last admitted (window position cnt - 1) and next pending (position cnt)
+        const uint32_t jl = cnt ? cnt - 1u : 0u, jn = cnt < (uint32_t)GW ? cnt : (uint32_t)GW - 1u;
+        uint32_t el = v[0], en = v[0];
+#pragma unroll
+        for (int k = 1; k < WA; ++k) {
+          if (jl % WA == (uint32_t)k) el = v[k];
+          if (jn % WA == (uint32_t)k) en = v[k];
+        }
+        const uint32_t lv = __shfl_sync(FULL, el, sg.grp * GL + (int)(jl / WA), LPS);
+        const uint32_t nx = __shfl_sync(FULL, en, sg.grp * GL + (int)(jn / WA), LPS);
         if (run) {
           next_arr = nx;
           if (cnt) last = lv;
           tail += cnt;
           if (sg.sbits(badb)) status = ES_ERR_UNSORTED;
         }
-        more = __any_sync(FULL, run && status == ES_OK && cnt == (uint32_t)GL);
+        more = __any_sync(FULL, run && status == ES_OK && cnt == (uint32_t)GW);
       }
       // the next decision's first admission round reads this window
-      if (run && tail + sg.gl < n) win = ldg_u32(Aq + tail + sg.gl);
+      if (run) {
+#pragma unroll
+        for (int k = 0; k < WA; ++k) {
+          const uint32_t idx = tail + (uint32_t)(sg.gl * WA + k);
+          if (idx < n) win[k] = ldg_u32(Aq + idx);
+        }
+      }
       // keep the next PF_LINES 128-byte lines of this model's arrivals in L1
       // (the admission loads above are the head of the per-decision chain)
       if (run && sg.gl < PF_LINES) {
