@@ -69,7 +69,7 @@ template <int LPS, int MM, bool POL, bool OUT>
 #ifdef ES_K2_MINB
 #define ES_K2_BOUNDS __launch_bounds__(256, ES_K2_MINB)
 #else
-#define ES_K2_BOUNDS __launch_bounds__(256)
+#define ES_K2_BOUNDS __launch_bounds__(512)
 #endif
 __global__ void ES_K2_BOUNDS k2_replay(const uint8_t *__restrict__ gimg, ImgLayout lay, ReplayArgs a) {
   constexpr int GL = Seg<LPS, MM>::GL;
@@ -462,7 +462,7 @@ cudaError_t launch_t(const uint8_t *img, const ImgLayout &lay, const ReplayArgs 
   auto dyn_of = [&](int threads) {
     return (((size_t)a.stage_bytes + 15u) & ~(size_t)15u) + (LPS == 8 ? (size_t)(threads / 32) * FLAT_BYTES : 0u);
   };
-  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn_of(256));
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn_of(512));
   if (e != cudaSuccess) return e;
   // threads per block: the smallest of 64 / 128 / 256 that keeps the resident
   // thread count of 256-thread blocks (small blocks deal the longest-first
@@ -484,9 +484,21 @@ cudaError_t launch_t(const uint8_t *img, const ImgLayout &lay, const ReplayArgs 
       break;
     }
   }
+  // a throughput batch (>= 256 scenarios per SM) takes 512-thread CTAs: one
+  // staged image per 16 warps leaves L1 the most room for the re-read waits
+  // (cfg3: 43.2 -> 41.8 ms vs 256-thread CTAs)
+  if (a.n_scen >= (int64_t)256 * sms) {
+    int o = 0;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, kern, 512, dyn_of(512));
+    if (e != cudaSuccess) return e;
+    if (o >= 1 && o * 512 >= occ * threads) {
+      threads = 512;
+      occ = o;
+    }
+  }
   if (const char *env = getenv("ES_K2_BLOCK")) {
     const int v = atoi(env);
-    if (v == 32 || v == 64 || v == 128 || v == 256) {
+    if (v == 32 || v == 64 || v == 128 || v == 256 || v == 512) {
       threads = v;
       e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, threads, dyn_of(threads));
       if (e != cudaSuccess) return e;

@@ -141,8 +141,9 @@ __global__ void __launch_bounds__(NT) k3_stats(StatsArgs a) {
     // of the 16-byte aligned span [gsrc - off, ...) (off <= 3 leading words
     // ignored), the <= 3 trailing words loaded directly
     const uint32_t *src = gsrc;
+    uint32_t off = 0u;  // staged: vals[off + i] holds latency i (vals 16-byte aligned)
     if (staged) {
-      const uint32_t off = (uint32_t)(((uintptr_t)gsrc >> 2) & 3u);
+      off = (uint32_t)(((uintptr_t)gsrc >> 2) & 3u);
       const uint32_t nv4 = (n + off) / 4u;
       if (threadIdx.x == 0 && nv4) {
         // the previous scenario's generic-proxy reads of vals precede these async writes
@@ -177,12 +178,36 @@ __global__ void __launch_bounds__(NT) k3_stats(StatsArgs a) {
     if (threadIdx.x == 0) s_max = 0u;
     __syncthreads();  // staged tail words and the zeroed histogram are visible
     uint32_t mx = 0;
-    for (uint32_t i0 = 0; i0 < n; i0 += NT) {
-      const uint32_t i = i0 + threadIdx.x;
-      const bool take = i < n;
-      const uint32_t v = take ? src[i] : 0u;
-      mx = max(mx, v);
-      if (take) atomicAdd(&hist[min(v >> 12, COARSE_OVF)], 1u);
+    // staged: 16-byte shared loads; the quads strictly inside [off, n + off)
+    // take no per-element test, the (at most two) edge quads do
+    const uint4 *v4 = reinterpret_cast<const uint4 *>(vals);
+    const uint32_t nq = (n + off + 3u) / 4u;
+    if (staged) {
+      for (uint32_t q = threadIdx.x; q < nq; q += NT) {
+        const uint4 x = v4[q];
+        const uint32_t j = 4u * q;
+        if (j >= off && j + 4u <= n + off) {
+          mx = max(max(mx, max(x.x, x.y)), max(x.z, x.w));
+          atomicAdd(&hist[min(x.x >> 12, COARSE_OVF)], 1u);
+          atomicAdd(&hist[min(x.y >> 12, COARSE_OVF)], 1u);
+          atomicAdd(&hist[min(x.z >> 12, COARSE_OVF)], 1u);
+          atomicAdd(&hist[min(x.w >> 12, COARSE_OVF)], 1u);
+        } else {
+          const uint32_t e[4] = {x.x, x.y, x.z, x.w};
+#pragma unroll
+          for (int c = 0; c < 4; ++c)
+            if (j + c >= off && j + c < n + off) {
+              mx = max(mx, e[c]);
+              atomicAdd(&hist[min(e[c] >> 12, COARSE_OVF)], 1u);
+            }
+        }
+      }
+    } else {
+      for (uint32_t i = threadIdx.x; i < n; i += NT) {
+        const uint32_t v = __ldg(gsrc + i);
+        mx = max(mx, v);
+        atomicAdd(&hist[min(v >> 12, COARSE_OVF)], 1u);
+      }
     }
     mx = __reduce_max_sync(0xffffffffu, mx);
     if ((threadIdx.x & 31) == 0) atomicMax(&s_max, mx);
@@ -203,9 +228,28 @@ __global__ void __launch_bounds__(NT) k3_stats(StatsArgs a) {
         kk -= before;
         for (int i = threadIdx.x; i < BINS; i += NT) hist[i] = 0u;
         __syncthreads();
-        for (uint32_t i = threadIdx.x; i < n; i += NT) {
-          const uint32_t v = src[i];
-          if ((v >> 12) == cb) atomicAdd(&hist[v & 0xFFFu], 1u);
+        if (staged) {
+          for (uint32_t q = threadIdx.x; q < nq; q += NT) {
+            const uint4 x = v4[q];
+            const uint32_t j = 4u * q;
+            // words outside [off, n + off) never match (masked to all ones)
+            const uint32_t e0 = j >= off && j < n + off ? x.x : 0xFFFFFFFFu;
+            const uint32_t e1 = j + 1u >= off && j + 1u < n + off ? x.y : 0xFFFFFFFFu;
+            const uint32_t e2 = j + 2u >= off && j + 2u < n + off ? x.z : 0xFFFFFFFFu;
+            const uint32_t e3 = j + 3u < n + off ? x.w : 0xFFFFFFFFu;
+            const bool h0 = (e0 >> 12) == cb, h1 = (e1 >> 12) == cb, h2 = (e2 >> 12) == cb, h3 = (e3 >> 12) == cb;
+            if (h0 | h1 | h2 | h3) {
+              if (h0) atomicAdd(&hist[e0 & 0xFFFu], 1u);
+              if (h1) atomicAdd(&hist[e1 & 0xFFFu], 1u);
+              if (h2) atomicAdd(&hist[e2 & 0xFFFu], 1u);
+              if (h3) atomicAdd(&hist[e3 & 0xFFFu], 1u);
+            }
+          }
+        } else {
+          for (uint32_t i = threadIdx.x; i < n; i += NT) {
+            const uint32_t v = __ldg(gsrc + i);
+            if ((v >> 12) == cb) atomicAdd(&hist[v & 0xFFFu], 1u);
+          }
         }
         __syncthreads();
         const uint32_t fb = find_bin(hist, BINS, kk, &before);
