@@ -464,6 +464,12 @@ __global__ void __launch_bounds__(TMA_NW * 32, 1) k1s_stream_tma(const uint8_t *
     hi = min(hi, lo + step);
   }
   pdl_wait();  // k1s_prep's snapshot flags
+  if ((int64_t)*a.slow_n == a.n) {
+    // every snapshot takes the clip path (k1s_stream_slow reads its live
+    // windows): nothing to stream here; drain the pieces already in flight
+    for (int64_t k = 0; k < min((int64_t)rg.nsl - 1, npieces); ++k) mbar_wait(bars + 8u * (uint32_t)k, 0u);
+    return;
+  }
   constexpr int32_t BIG = 0x3FFFFFFF;
   const int32_t rend_full = (int32_t)(4 * (min(v1, nfull) - v0));  // fast windows end here
   int64_t qi = lo, s_cur = lo / M;
