@@ -266,7 +266,7 @@ def bench_k1(es, dev, stream, rank, depth=4096):
     n0 = (q_off.size - 1) // 8 // tiles
     return k1_line(es, h, 8, q_off[:n0 * 8 + 1], w0, tiles, None, x_c, dev, stream,
                    f"5-C shape: 8 DNNs x 5 exits x batch 1-32, depth U[0,{depth}] per model, all tasks live",
-                   "k1 call: k1s_prep + k1s_stream_tma + k1s_stream_slow + k1s_finish", "k1_call")
+                   "k1 call: k1s_prep + k1s_stream_tma + k1s_clip + k1s_finish", "k1_call")
 
 
 def bench_k1_clip(es, dev, stream, rank, depth=4096):
@@ -286,12 +286,10 @@ def bench_k1_clip(es, dev, stream, rank, depth=4096):
                    "the general clip path", "k1 call (clip path)", "k1_clip")
 
 
-def bench_k1_harvested(es, engine, dev, stream, rank, n_scen=512, tiles=8):
-    """K1 on queue snapshots harvested at the decision instants of cfg3
-    replays ('harvested config-3 snapshots'): n_scen cfg3
-    scenarios replayed by K2 with the decision log on, every decision's queue
-    state rebuilt on the host (inputs.harvest_snapshots, pure indexing), nine
-    SLO configs mixed by the snapshots' cfg index -- the warp-segment mapping."""
+def k1_harvested_batch(es, engine, dev, stream, rank, n_scen=512):
+    """The harvested cfg3 snapshots (host arrays) and a profile handle: n_scen
+    cfg3 scenarios replayed by K2 with the decision log on, every decision's
+    queue state rebuilt on the host (inputs.harvest_snapshots, pure indexing)."""
     import torch
     import inputs
     w = inputs.workload("cfg3", scen_ids=np.arange(rank * n_scen, (rank + 1) * n_scen))
@@ -306,11 +304,19 @@ def bench_k1_harvested(es, engine, dev, stream, rank, n_scen=512, tiles=8):
                                              o["dec_m"].cpu().numpy(), o["dec_B"].cpu().numpy())
     del o, d
     x_c = [es.es_get_tables(h, k)["x_c"] for k in range(len(w.cfgs))]
+    return h, q_off, w0, ci, x_c
+
+
+def bench_k1_harvested(es, engine, dev, stream, rank, n_scen=512, tiles=8, batch=None):
+    """K1 on queue snapshots harvested at the decision instants of cfg3
+    replays ('harvested config-3 snapshots', k1_harvested_batch),
+    nine SLO configs mixed by the snapshots' cfg index."""
+    h, q_off, w0, ci, x_c = batch or k1_harvested_batch(es, engine, dev, stream, rank, n_scen)
     live_per = float(np.mean(np.diff(q_off[::8].astype(np.int64))))
     return k1_line(es, h, 8, q_off, w0, tiles, ci, x_c, dev, stream,
                    f"cfg3 harvested: every decision instant of {n_scen} cfg3 scenarios (8 DNNs x 5 exits x batch "
                    f"1-32, 9 SLOs), {live_per:.1f} queued tasks per snapshot on average",
-                   "k1 call (warp-segment mapping)", "k1_harvested")
+                   "k1 call (thread per snapshot)", "k1_harvested")
 
 
 def run_reference(args, rank, world):

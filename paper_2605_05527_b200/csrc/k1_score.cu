@@ -10,6 +10,7 @@
 // snapshots.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdlib>
 #include <cstring>
 
@@ -30,6 +31,11 @@ struct ScoreArgs {
   uint8_t *flags;
   uint64_t *cand;
   DevStatus *dstat;
+  uint32_t stage_bytes;  // image prefix staged per CTA (lay.bytes, or lay.core_bytes: H read from global)
+  // clip-path hand-over from k1_thread to k1_score: list of snapshot indices
+  // and its length (device); k1_score walks list[0 .. *list_n) when non-null
+  uint32_t *list;
+  unsigned long long *list_n;
 };
 
 template <int LPS, int MM, bool POL>
@@ -38,16 +44,18 @@ __global__ void __launch_bounds__(256) k1_score(const uint8_t *__restrict__ gimg
   constexpr int SPW = 32 / LPS;  // segments per warp
   extern __shared__ __align__(16) uint8_t smem[];
   __shared__ uint64_t mbar;
-  stage_image(smem, gimg, lay.bytes, &mbar);
-  const SmemProf P = smem_prof(smem, lay);
+  stage_image(smem, gimg, a.stage_bytes, &mbar);
+  SmemProf P = smem_prof(smem, lay);
+  if (a.stage_bytes < lay.bytes) P.hb = gimg;  // H tables stay in global memory (L1-cached)
   const Seg<LPS, MM> sg;
   const int g = sg.grp;
   const int M = P.M;
   const int64_t wid = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  for (int64_t s0 = wid * SPW; s0 < a.n; s0 += nw * SPW) {  // warp-uniform loop
-    const int64_t s = s0 + sg.seg;
-    const bool live_s = s < a.n;
+  const int64_t nitems = a.list ? (int64_t)*a.list_n : a.n;  // k1_thread's clip-path list, or every snapshot
+  for (int64_t s0 = wid * SPW; s0 < nitems; s0 += nw * SPW) {  // warp-uniform loop
+    const bool live_s = s0 + sg.seg < nitems;
+    const int64_t s = !live_s ? 0 : a.list ? (int64_t)a.list[s0 + sg.seg] : s0 + sg.seg;
     const int k = live_s ? (a.cfg_idx ? (int)a.cfg_idx[s] : 0) : 0;
     const bool cfg_ok = k < P.ncfg;
     const SmemCfg C = smem_cfg(P, cfg_ok ? k : 0);
@@ -135,10 +143,10 @@ __global__ void __launch_bounds__(256) k1_score(const uint8_t *__restrict__ gimg
 template <int LPS, int MM>
 cudaError_t launch_t(const uint8_t *img, const ImgLayout &lay, const ScoreArgs &a, cudaStream_t st, int sms) {
   auto kern = lay.pol_mask == (1u << ES_POLICY_EDGESERVING) ? k1_score<LPS, MM, false> : k1_score<LPS, MM, true>;
-  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lay.bytes);
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)a.stage_bytes);
   if (e != cudaSuccess) return e;
   int occ = 0;
-  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 256, lay.bytes);
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 256, a.stage_bytes);
   if (e != cudaSuccess) return e;
   if (occ < 1) return cudaErrorInvalidConfiguration;
   constexpr int SEG_PER_BLOCK = 256 / LPS;
@@ -146,7 +154,7 @@ cudaError_t launch_t(const uint8_t *img, const ImgLayout &lay, const ScoreArgs &
   const int64_t cap = (int64_t)sms * occ;
   if (blocks > cap) blocks = cap;
   if (blocks < 1) blocks = 1;
-  kern<<<(unsigned)blocks, 256, lay.bytes, st>>>(img, lay, a);
+  kern<<<(unsigned)blocks, 256, a.stage_bytes, st>>>(img, lay, a);
   return cudaGetLastError();
 }
 
@@ -158,273 +166,365 @@ cudaError_t launch_lps(const uint8_t *img, const ImgLayout &lay, const ScoreArgs
 }
 
 // ---------------------------------------------------------------------------
-// Deep snapshots: one CTA (256 threads) per snapshot streams every live wait
-// with coalesced loads; per-queue state and the candidates live in shared
-// memory.  Same integers as k1_score (decide.cuh); only the mapping differs.
-constexpr int BT = 128;
-constexpr int BW = BT / 32;
+// Short snapshots under Algorithm 1: one THREAD per snapshot (k1_thread).
+// A warp segment spends warp-wide shuffles and reductions on a handful of
+// waits (harvested cfg3 states: 33 waits over 8 queues on average, median
+// queue 2), so here each lane owns a snapshot's decision logic:
+//   per queue q: Eq. 5 (bidx, Q8) and Eq. 6 (binary search on the strictly
+//   increasing exit latencies, Q2); S_q(m) = floor(H(L_m) (tot - srv_m) /
+//   2^28) and the Eq. 7 argmin (S, m) (Q3) -- the fast path of decide.cuh
+//   (same integers), valid when every head wait is below x_c - max L.
+// The sums come from one balanced pass of the whole warp: the waits of the
+// warp's 32 consecutive snapshots are one contiguous region, read as 16-byte
+// vectors (8 waits per lane, 256 per trip) whatever the queue-length mix; G(w)
+// (Q5) of every wait with the SLO's tables (a warp whose snapshots mix SLOs
+// takes the per-lane loop below), an exclusive running sum E over the region
+// into shared memory (chunks of `cap` positions), and each lane reads E at its
+// queues' boundaries:  tot = E(end_M) - E(start_0),  srv_m = E(start_m +
+// min(B*_m, len_m)) - E(start_m)  (own served head).  Read-window check
+// (Q24): a wait above its predecessor inside a queue (queue starts marked in a
+// per-chunk bitmap) sends the warp to the per-lane loop, which flags it.
+// A snapshot with a head at or past x_c - max L (some task may clip) is
+// appended to a list that the warp-segment kernel (k1_score, general clip
+// path) scores afterwards.
+constexpr int K1T_THREADS = 512;
+constexpr int K1T_WARPS = K1T_THREADS / 32;
 
-__device__ __forceinline__ uint64_t warp_sum64(uint64_t v) {
-#pragma unroll
-  for (int o = 16; o >= 1; o >>= 1) v += __shfl_xor_sync(FULL, v, o);
+__device__ __forceinline__ uint32_t lds32(uint32_t a) {
+  uint32_t v;
+  asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(a));
   return v;
 }
-__device__ __forceinline__ uint32_t warp_sum32(uint32_t v) { return redux_add(v); }
+__device__ __forceinline__ uint64_t lds64(uint32_t a) {
+  uint64_t v;
+  asm volatile("ld.shared.u64 %0, [%1];" : "=l"(v) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ void sts128(uint32_t a, uint64_t x, uint64_t y) {
+  asm volatile("st.shared.v2.u64 [%0], {%1, %2};" ::"r"(a), "l"(x), "l"(y) : "memory");
+}
+
+// G(w) with 32-bit shared addresses: v4 = 4 (w + r) (exact: x_c + 1024 < 2^30
+// for tau <= 2^20, Q25); the A index is clamped (an inverted input is flagged
+// and its value unused)
+struct GSh {
+  uint32_t sA, sBt, r4, nA1;
+  __device__ __forceinline__ uint32_t operator()(uint32_t w) const {
+    const uint32_t v4 = w * 4u + r4;
+    const uint32_t h = min(v4 >> (SBITS + 2), nA1);
+    return (uint32_t)(((uint64_t)lds32(sA + 4u * h) * (uint64_t)lds32(sBt + (v4 & (4u * S - 4u)))) >> F);
+  }
+};
 
 template <int MM>
-__global__ void __launch_bounds__(BT) k1_block(const uint8_t *__restrict__ gimg, ImgLayout lay, ScoreArgs a) {
+__global__ void __launch_bounds__(K1T_THREADS, 1) k1_thread(const uint8_t *__restrict__ gimg, ImgLayout lay,
+                                                           ScoreArgs a, uint32_t cap) {
   extern __shared__ __align__(16) uint8_t smem[];
   __shared__ uint64_t mbar;
-  __shared__ uint64_t s_lo[MM], s_H[MM], s_srv[MM], s_S[MM];
-  __shared__ uint32_t s_len[MM], s_wmax[MM], s_c[MM], s_B[MM], s_e[MM], s_L[MM], s_thr[MM], s_feas[MM];
-  __shared__ uint64_t s_redU[BW][MM];
-  __shared__ uint32_t s_redK[BW][MM];
-  __shared__ int s_bad, s_fast;
-  stage_image(smem, gimg, lay.bytes, &mbar);
-  const SmemProf P = smem_prof(smem, lay);
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  stage_image(smem, gimg, a.stage_bytes, &mbar);
+  SmemProf P = smem_prof(smem, lay);
+  if (a.stage_bytes < lay.bytes) P.hb = gimg;  // H tables stay in global memory (L1-cached)
   const int M = P.M;
-  // the next snapshot's CSR entries and head waits are prefetched into
-  // registers of threads 0..M-1 while the current one streams
-  auto fetch = [&](int64_t ss, int &kk, uint64_t &lo, uint32_t &len, uint32_t &wm) {
-    kk = 0;
-    lo = 0;
-    len = 0;
-    wm = 0;
-    if (ss < a.n && tid < M) {
-      kk = a.cfg_idx ? (int)a.cfg_idx[ss] : 0;
-      if (kk < P.ncfg) {
-        lo = a.q_off[ss * M + tid];
-        len = (uint32_t)(a.q_off[ss * M + tid + 1] - lo);
-        wm = len ? __ldg(a.waits + lo) : 0u;
-      }
-    }
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(smem);
+  // this warp's scratch: E [cap + 4] u64, then the queue-start bitmap [cap / 32]
+  const uint32_t sE = sbase + ((a.stage_bytes + 127u) & ~127u) + (uint32_t)wib * (cap * 8u + 32u + cap / 8u);
+  const uint32_t sBits = sE + cap * 8u + 32u;
+  const int64_t nwarps = (int64_t)gridDim.x * K1T_WARPS;
+  auto out_empty = [&](int64_t s, uint8_t flag) {
+    a.m[s] = 0; a.e[s] = 0; a.B[s] = 0; a.L[s] = 0; a.S[s] = 0;
+    a.flags[s] = flag;
+    if (a.cand)
+      for (int q = 0; q < M; ++q) a.cand[s * M + q] = ~0ull;
   };
-  int nk;
-  uint64_t nlo;
-  uint32_t nlen, nwm;
-  fetch(blockIdx.x, nk, nlo, nlen, nwm);
-  for (int64_t s = blockIdx.x; s < a.n; s += gridDim.x) {
-    const int k = a.cfg_idx ? (int)a.cfg_idx[s] : 0;
+  // each warp takes one contiguous block of snapshots, 32 per iteration: the
+  // next iteration's CSR rows, SLO indices and waits follow this one's, so
+  // they are prefetched into L2 while this one is scored
+  const int64_t per = ((a.n + nwarps - 1) / nwarps + 31) & ~31ll;
+  const int64_t wbeg = ((int64_t)blockIdx.x * K1T_WARPS + wib) * per, wend = min(wbeg + per, a.n);
+  for (int64_t s0 = wbeg; s0 < wend; s0 += 32) {  // warp-uniform
+    const int64_t s = s0 + lane;
+    const bool live = s < wend;
+    const int k = live ? (a.cfg_idx ? (int)a.cfg_idx[s] : 0) : 0;
     const bool cfg_ok = k < P.ncfg;
     const SmemCfg C = smem_cfg(P, cfg_ok ? k : 0);
-    if (tid < MM) {
-      s_lo[tid] = nlo;
-      s_len[tid] = nlen;
-      s_wmax[tid] = nwm;
-      s_c[tid] = 0;
-      s_srv[tid] = 0;
-    }
-    fetch(s + gridDim.x, nk, nlo, nlen, nwm);  // consumed next iteration
-    if (tid == 0) {
-      s_bad = cfg_ok ? 0 : 1;
-      s_fast = 1;
-    }
-    __syncthreads();
-    // clipped-for-everyone prefix of queue `warp`: 32-ary search on the
-    // non-increasing waits (counted, never read)
-    for (int qs = warp; qs < M; qs += BW) {  // warp-uniform
-      if (!(s_len[qs] && s_wmax[qs] >= C.x_c)) continue;
-      const uint32_t *W = a.waits + s_lo[qs];
-      uint32_t plo = 0, phi = s_len[qs];  // w[plo] >= x_c, w[phi] < x_c (phi == len: sentinel)
-      while (phi - plo > 1u) {  // warp-uniform
-        const uint32_t nin = phi - plo - 1u;
-        const uint32_t q = plo + 1u + (uint32_t)(((uint64_t)(lane + 1) * nin) / 33u);
-        const bool pr = __ldg(W + (q < phi ? q : phi - 1u)) >= C.x_c;
-        const uint32_t cnt = __popc(__ballot_sync(FULL, pr));
-        const uint32_t q_lo = __shfl_sync(FULL, q, cnt ? cnt - 1 : 0);
-        const uint32_t q_hi = __shfl_sync(FULL, q, cnt < 32 ? cnt : 31);
-        if (cnt) plo = q_lo;
-        if (cnt < 32u) phi = q_hi;
-      }
-      if (lane == 0) s_c[qs] = phi;
-    }
-    // Eq. 5-6 per candidate
-    if (tid < M && s_len[tid]) {
-      const uint32_t len = s_len[tid];
-      const uint32_t cap = len < C.b_max ? len : C.b_max;
-      const uint32_t bi = P.sm[C.off_bidx + cap];
-      const uint32_t mbits = P.mask[tid];
-      const uint32_t *row = P.lat + (size_t)tid * P.E * P.nb + bi;
-      int best = -1;
-      for (int e = 0; e < P.E; ++e)
-        if (((mbits >> e) & 1u) && (uint64_t)s_wmax[tid] + row[e * P.nb] <= (uint64_t)C.tau) best = e;
-      const uint32_t e = best >= 0 ? (uint32_t)best : (uint32_t)(__ffs(mbits) - 1);
-      const uint32_t L = row[e * P.nb];
-      s_B[tid] = P.bs[bi];
-      s_e[tid] = e;
-      s_L[tid] = L;
-      s_feas[tid] = best >= 0;
-      s_thr[tid] = L < C.x_c ? C.x_c - L : 0u;
-      s_H[tid] = L < C.x_c ? reinterpret_cast<const uint64_t *>(P.hb + C.off_H)[((size_t)tid * P.E + e) * P.nb + bi]
-                           : 0ull;
-      if (s_wmax[tid] >= C.fast_lim) s_fast = 0;
-    }
-    __syncthreads();
-    const bool fast = s_fast != 0;
-    uint64_t U[MM];
-    uint32_t K[MM];
+    // CSR row and head waits: all loads independent
+    uint64_t off[MM + 1];
 #pragma unroll
-    for (int m = 0; m < MM; ++m) {
-      U[m] = 0ull;
-      K[m] = 0u;
+    for (int q = 0; q <= MM; ++q) off[q] = live && q <= M ? __ldg(a.q_off + s * M + q) : 0ull;
+    // the region of this iteration's waits [R0, R1): contiguous (consecutive snapshots)
+    const uint64_t R0 = __shfl_sync(FULL, off[0], 0);
+    const int ll = 31 - __clz(__ballot_sync(FULL, live));
+    uint64_t R1 = 0ull;
+#pragma unroll
+    for (int q = 0; q <= MM; ++q)
+      if (q == M) R1 = __shfl_sync(FULL, off[q], ll);
+    if (s0 + 32 < wend) {  // L2 prefetch of the next iteration: CSR rows, SLO indices, first 8 KB of waits
+      const char *nq = reinterpret_cast<const char *>(a.q_off + (s0 + 32) * M);
+      if ((uint32_t)lane * 128u < 32u * 8u * (uint32_t)M + 8u) asm volatile("prefetch.global.L2 [%0];" ::"l"(nq + 128 * lane));
+      if (lane == 31 && a.cfg_idx) asm volatile("prefetch.global.L2 [%0];" ::"l"(a.cfg_idx + s0 + 32));
+      const char *nw = reinterpret_cast<const char *>(a.waits + R1);
+      asm volatile("prefetch.global.L2 [%0];" ::"l"(nw + 128 * lane));
+      asm volatile("prefetch.global.L2 [%0];" ::"l"(nw + 128 * (lane + 32)));
     }
-    uint64_t tot = 0;
-    bool bad = false;
-    // the two loops are separate so the compiler cannot if-convert both bodies
-    if (fast) {
-    for (int q = 0; q < M; ++q) {
-      const uint32_t len = s_len[q], c0 = s_c[q], Bq = s_B[q];
-      const uint32_t *W = a.waits + s_lo[q];
-      // each warp streams a contiguous slice of the live window, UNR coalesced
-      // 32-wide loads in flight; the neighbour check carries lane 31's value
-      constexpr int UNR = 4;
-      const uint32_t nlive = len > c0 ? len - c0 : 0u;
-      const uint32_t per = ((nlive + BW * 32u - 1u) / (BW * 32u)) * 32u;  // slice, multiple of 32
-      const uint32_t beg = c0 + warp * per, end = min(beg + per, len);
-      uint32_t carry = (beg > c0 && beg < end) ? __ldg(W + beg - 1) : 0xFFFFFFFFu;
-      for (uint32_t p0 = beg; p0 < end; p0 += UNR * 32u) {  // warp-uniform trip count
-        uint32_t wv[UNR];
+    uint32_t head[MM];
+    bool slow = false, any = false;
 #pragma unroll
-        for (int jj = 0; jj < UNR; ++jj) {
-          const uint32_t p = p0 + jj * 32u + lane;
-          wv[jj] = p < end ? __ldg(W + p) : 0u;
-        }
-#pragma unroll
-        for (int jj = 0; jj < UNR; ++jj) {
-          const uint32_t p = p0 + jj * 32u + lane;
-          const uint32_t w = wv[jj];
-          const bool valid = p < end;
-          uint32_t prev = __shfl_up_sync(FULL, w, 1);
-          if (lane == 0) prev = carry;
-          carry = __shfl_sync(FULL, w, 31);
-          if (valid && (w > prev || w >= C.x_c)) bad = true;  // read-window validation (Q7, Q24)
-          if (!valid) continue;
-          const uint32_t gw = G_of(P, C, w);
-          tot += gw;
-          if (p < Bq) atomicAdd(reinterpret_cast<unsigned long long *>(&s_srv[q]), (unsigned long long)gw);
-        }
-      }
+    for (int q = 0; q < MM; ++q) {
+      const bool has = q < M && off[q + 1] > off[q];
+      head[q] = has ? __ldg(a.waits + off[q]) : 0u;
+      slow |= has && head[q] >= C.fast_lim;
+      any |= has;
     }
-    } else {
-      uint32_t thr_r[MM];
-#pragma unroll
-      for (int m = 0; m < MM; ++m) thr_r[m] = m < M ? s_thr[m] : 0xFFFFFFFFu;
-    for (int q = 0; q < M; ++q) {
-      const uint32_t len = s_len[q], c0 = s_c[q], Bq = s_B[q];
-      const uint32_t *W = a.waits + s_lo[q];
-      // each warp streams a contiguous slice of the live window, UNR coalesced
-      // 32-wide loads in flight; the neighbour check carries lane 31's value
-      constexpr int UNR = 4;
-      const uint32_t nlive = len > c0 ? len - c0 : 0u;
-      const uint32_t per = ((nlive + BW * 32u - 1u) / (BW * 32u)) * 32u;  // slice, multiple of 32
-      const uint32_t beg = c0 + warp * per, end = min(beg + per, len);
-      uint32_t carry = (beg > c0 && beg < end) ? __ldg(W + beg - 1) : 0xFFFFFFFFu;
-      for (uint32_t p0 = beg; p0 < end; p0 += UNR * 32u) {  // warp-uniform trip count
-        uint32_t wv[UNR];
-#pragma unroll
-        for (int jj = 0; jj < UNR; ++jj) {
-          const uint32_t p = p0 + jj * 32u + lane;
-          wv[jj] = p < end ? __ldg(W + p) : 0u;
-        }
-#pragma unroll
-        for (int jj = 0; jj < UNR; ++jj) {
-          const uint32_t p = p0 + jj * 32u + lane;
-          const uint32_t w = wv[jj];
-          const bool valid = p < end;
-          uint32_t prev = __shfl_up_sync(FULL, w, 1);
-          if (lane == 0) prev = carry;
-          carry = __shfl_sync(FULL, w, 31);
-          if (valid && (w > prev || w >= C.x_c)) bad = true;  // read-window validation (Q7, Q24)
-          if (!valid) continue;
-          const uint32_t gw = G_of(P, C, w);
-#pragma unroll
-          for (int m = 0; m < MM; ++m) {
-            if (m == q && p < Bq) continue;  // candidate m's own served tasks
-            if (w >= thr_r[m]) K[m] += 1u;
-            else U[m] += gw;
-          }
-        }
-      }
-    }
-    }
-    if (__any_sync(FULL, bad) && lane == 0) s_bad = 1;
-    if (fast) {
-      tot = warp_sum64(tot);
-      if (lane == 0) s_redU[warp][0] = tot;
-    } else {
-#pragma unroll
-      for (int m = 0; m < MM; ++m) {
-        const uint64_t u = warp_sum64(U[m]);
-        const uint32_t kk = warp_sum32(K[m]);
-        if (lane == 0) {
-          s_redU[warp][m] = u;
-          s_redK[warp][m] = kk;
-        }
-      }
-    }
-    __syncthreads();
-    if (tid < M) {
-      uint64_t S = ~0ull;
-      if (s_len[tid]) {
-        uint64_t u = 0, kk = 0;
-        if (fast) {
-          for (int w = 0; w < BW; ++w) u += s_redU[w][0];
-          u -= s_srv[tid];
-        } else {
-          for (int w = 0; w < BW; ++w) {
-            u += s_redU[w][tid];
-            kk += s_redK[w][tid];
-          }
-          uint32_t cpre = 0;
-          for (int q = 0; q < M; ++q) cpre += s_c[q];
-          const uint32_t cB = s_c[tid] < s_B[tid] ? s_c[tid] : s_B[tid];
-          kk += cpre - cB;
-        }
-        const uint64_t H = s_H[tid];
-        const uint64_t lo = H * u, hi = __umul64hi(H, u);
-        S = C.C_q * kk + ((hi << (64 - F)) | (lo >> F));
-      }
-      s_S[tid] = S;
-    }
-    __syncthreads();
-    if (tid == 0) {
-      int best = -1;
-      for (int m = 0; m < M; ++m)
-        if (s_len[m] && (best < 0 || s_S[m] < s_S[best])) best = m;  // (S, m): lowest m on ties
-      if (s_bad || best < 0) {
-        a.m[s] = 0; a.e[s] = 0; a.B[s] = 0; a.L[s] = 0; a.S[s] = 0;
-        a.flags[s] = s_bad ? ES_FLAG_BAD_INPUT : ES_FLAG_NO_WORK;
-        if (!cfg_ok && atomicCAS(&a.dstat->code, 0u, (uint32_t)ES_ERR_ARG) == 0u) a.dstat->item = s;
+    bool active = false;
+    if (live) {
+      if (!cfg_ok) {
+        out_empty(s, ES_FLAG_BAD_INPUT);
+        if (atomicCAS(&a.dstat->code, 0u, (uint32_t)ES_ERR_ARG) == 0u) a.dstat->item = s;
+      } else if (slow) {  // some task may clip: the general path (k1_score on the list)
+        a.list[atomicAdd(a.list_n, 1ull)] = (uint32_t)s;
+      } else if (!any) {
+        out_empty(s, ES_FLAG_NO_WORK);
       } else {
-        a.m[s] = (uint8_t)best;
-        a.e[s] = (uint8_t)s_e[best];
-        a.B[s] = (uint16_t)s_B[best];
-        a.L[s] = s_L[best];
-        a.S[s] = s_S[best];
-        a.flags[s] = s_feas[best] ? ES_FLAG_FEASIBLE : 0u;
+        active = true;
       }
     }
-    if (a.cand && tid < M) a.cand[s * M + tid] = (s_bad || !s_len[tid]) ? ~0ull : s_S[tid];
-    __syncthreads();
+    const unsigned b_act = __ballot_sync(FULL, active);
+    if (b_act == 0u) continue;
+    // Eq. 5 / Eq. 6 of every queue (empty: 0xFFFFFFFF); nsv = min(B*, len)
+    uint32_t pk[MM], nsv[MM];  // pk = e | bi << 4 | feasible << 12
+#pragma unroll
+    for (int q = 0; q < MM; ++q) {
+      pk[q] = 0xFFFFFFFFu;
+      nsv[q] = 0u;
+      const uint32_t len = q < M ? (uint32_t)(off[q + 1] - off[q]) : 0u;
+      if (!active || !len) continue;
+      const uint32_t cap_b = len < C.b_max ? len : C.b_max;
+      const uint32_t bi = P.sm[C.off_bidx + cap_b];
+      nsv[q] = min((uint32_t)P.bs[bi], len);
+      const uint32_t *row = P.lat + (size_t)q * P.E * P.nb + bi;  // row[e * nb]
+      const uint32_t mbits = P.mask[q];
+      unsigned bits = 0u;
+      if (head[q] <= C.tau) {
+        const uint32_t lim = C.tau - head[q];
+        uint32_t c = 0u;
+        if (8 <= P.E && row[7 * P.nb] <= lim) c = 8u;
+        if (c + 4u <= (uint32_t)P.E && row[(c + 3u) * P.nb] <= lim) c += 4u;
+        if (c + 2u <= (uint32_t)P.E && row[(c + 1u) * P.nb] <= lim) c += 2u;
+        if (c + 1u <= (uint32_t)P.E && row[c * P.nb] <= lim) c += 1u;
+        bits = ((1u << c) - 1u) & mbits;
+      }
+      const uint32_t e = bits ? 31u - __clz(bits) : (uint32_t)(__ffs(mbits) - 1);
+      pk[q] = e | (bi << 4) | (bits ? 0x1000u : 0u);
+    }
+    uint64_t tot = 0ull, srv[MM];
+#pragma unroll
+    for (int q = 0; q < MM; ++q) srv[q] = 0ull;
+    bool bad = false;
+    // ---- the balanced pass: one SLO across the warp's active snapshots
+    const int kf = __shfl_sync(FULL, k, __ffs(b_act) - 1);
+    const uintptr_t a0 = reinterpret_cast<uintptr_t>(a.waits + R0);
+    const uint32_t mis = (uint32_t)((a0 & 15u) >> 2);  // waits before R0 in its 16-byte vector
+    bool flat = __all_sync(FULL, !active || k == kf) && R1 - R0 < (1ull << 30);
+    if (flat) {
+      const uint32_t *abase = reinterpret_cast<const uint32_t *>(a0 & ~(uintptr_t)15u);  // relative position 0
+      const uint32_t nrel = (uint32_t)(R1 - R0) + mis;
+      const SmemCfg Cf = smem_cfg(P, kf);
+      const GSh G{sbase + Cf.off_A, sbase + Cf.off_Bt, 4u * Cf.r, Cf.nA1};
+      uint64_t carry = 0ull;
+      uint32_t pcarry = 0xFFFFFFFFu;
+      bool inv = false;
+      for (uint32_t cb = 0; cb < nrel; cb += cap) {  // warp-uniform chunks
+        const uint32_t ce = min(cb + cap, nrel);
+        for (uint32_t j = lane; j < cap / 32u; j += 32u) asm volatile("st.shared.u32 [%0], 0;" ::"r"(sBits + 4u * j));
+        __syncwarp();
+        if (live) {  // queue starts of this chunk (no predecessor check there, Q24)
+#pragma unroll
+          for (int q = 0; q < MM; ++q) {
+            const uint32_t x = (uint32_t)(off[q] - R0) + mis;
+            if (q < M && x >= cb && x < ce)
+              asm volatile("red.shared.or.b32 [%0], %1;" ::"r"(sBits + 4u * ((x - cb) >> 5)), "r"(1u << ((x - cb) & 31u)));
+          }
+        }
+        __syncwarp();
+        for (uint32_t tb = cb; tb < ce; tb += 256u) {  // warp-uniform trips of 8 waits per lane
+          const uint32_t p = tb + 8u * (uint32_t)lane;
+          uint32_t w[8];
+          // positions outside [mis, nrel) (the region's edge vectors) are masked
+          const uint32_t vm = p >= mis && p + 8u <= nrel
+                                  ? 0xFFu
+                                  : (p + 8u <= mis || p >= nrel ? 0u
+                                                                : (0xFFu << (p < mis ? mis - p : 0u)) &
+                                                                      (0xFFu >> (p + 8u > nrel ? p + 8u - nrel : 0u)));
+          if (vm == 0xFFu) {
+            const uint4 v0 = __ldg(reinterpret_cast<const uint4 *>(abase + p));
+            const uint4 v1 = __ldg(reinterpret_cast<const uint4 *>(abase + p + 4u));
+            w[0] = v0.x; w[1] = v0.y; w[2] = v0.z; w[3] = v0.w;
+            w[4] = v1.x; w[5] = v1.y; w[6] = v1.z; w[7] = v1.w;
+          } else {
+#pragma unroll
+            for (int i = 0; i < 8; ++i) w[i] = (vm >> i) & 1u ? __ldg(abase + p + i) : 0u;
+          }
+          // Q24: a wait above its predecessor, except at a queue start
+          const uint32_t sb8 = (lds32(sBits + 4u * ((tb - cb) / 32u + (uint32_t)lane / 4u)) >> (8u * (lane & 3))) & 0xFFu;
+          uint32_t prev = __shfl_up_sync(FULL, w[7], 1);
+          if (lane == 0) prev = pcarry;
+          pcarry = __shfl_sync(FULL, w[7], 31);
+          uint32_t gt = w[0] > prev ? 1u : 0u;
+#pragma unroll
+          for (int i = 1; i < 8; ++i) gt |= w[i] > w[i - 1] ? 1u << i : 0u;
+          inv |= (gt & vm & ~sb8) != 0u;
+          uint64_t c[8];
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            const uint64_t g = (vm >> i) & 1u ? (uint64_t)G(w[i]) : 0ull;
+            c[i] = i ? c[i - 1] + g : g;
+          }
+          uint64_t sc = c[7];  // warp inclusive scan of the lane sums
+#pragma unroll
+          for (int o = 1; o < 32; o <<= 1) {
+            const uint64_t t = __shfl_up_sync(FULL, sc, o);
+            if (lane >= o) sc += t;
+          }
+          const uint64_t base = carry + sc - c[7];  // E at position p
+          const uint32_t ea = sE + 8u * (p - cb);
+          sts128(ea, base, base + c[0]);
+          sts128(ea + 16u, base + c[1], base + c[2]);
+          sts128(ea + 32u, base + c[3], base + c[4]);
+          sts128(ea + 48u, base + c[5], base + c[6]);
+          carry += __shfl_sync(FULL, sc, 31);
+        }
+        __syncwarp();
+        if (active) {  // this lane's queue boundaries inside the chunk
+#pragma unroll
+          for (int q = 0; q <= MM; ++q) {
+            if (q > M) continue;
+            const uint32_t x = (uint32_t)(off[q] - R0) + mis;
+            if (x >= cb && x < ce) {
+              const uint64_t e = lds64(sE + 8u * (x - cb));
+              if (q == 0) tot -= e;
+              if (q == M) tot += e;
+              if (q < M) srv[q] -= e;
+            }
+            if (q < M) {
+              const uint32_t x1 = x + nsv[q];
+              if (x1 >= cb && x1 < ce) srv[q] += lds64(sE + 8u * (x1 - cb));
+            }
+          }
+        }
+        __syncwarp();
+      }
+      if (active) {  // boundaries at the region's end: E = the final running sum
+#pragma unroll
+        for (int q = 0; q <= MM; ++q) {
+          if (q > M) continue;
+          const uint32_t x = (uint32_t)(off[q] - R0) + mis;
+          if (x == nrel) {
+            if (q == 0) tot -= carry;
+            if (q == M) tot += carry;
+            if (q < M) srv[q] -= carry;
+          }
+          if (q < M && x + nsv[q] == nrel) srv[q] += carry;
+        }
+      }
+      flat = !__any_sync(FULL, inv);  // an inversion: redo the warp per lane (flags it exactly)
+    }
+    if (!flat && active) {
+      // ---- per-lane loop (mixed SLOs or an inversion in the region)
+      tot = 0ull;
+      const GSh G{sbase + C.off_A, sbase + C.off_Bt, 4u * C.r, C.nA1};
+#pragma unroll
+      for (int q = 0; q < MM; ++q) {
+        srv[q] = 0ull;
+        const uint32_t len = q < M ? (uint32_t)(off[q + 1] - off[q]) : 0u;
+        if (!len) continue;
+        const uint32_t *W = a.waits + off[q];
+        uint32_t prev = head[q];
+        uint64_t Q = G(prev), sv = Q;  // nsv >= 1
+        for (uint32_t p = 1; p < len; ++p) {
+          const uint32_t w = __ldg(W + p);
+          bad |= w > prev;
+          prev = w;
+          const uint64_t g = G(w);
+          Q += g;
+          if (p < nsv[q]) sv += g;
+        }
+        tot += Q;
+        srv[q] = sv;
+      }
+    }
+    if (!active) continue;
+    if (bad) {
+      out_empty(s, ES_FLAG_BAD_INPUT);
+      continue;
+    }
+    // Eq. 3-4 on each candidate's predicted state, Eq. 7 argmin (S, m)
+    const uint64_t *Hq = reinterpret_cast<const uint64_t *>(P.hb + C.off_H);
+    uint64_t bS = ~0ull;
+    uint32_t bq = 0u, bpk = 0u;
+#pragma unroll
+    for (int q = 0; q < MM; ++q) {
+      if (q >= M) continue;
+      uint64_t Sv = ~0ull;
+      if (pk[q] != 0xFFFFFFFFu) {
+        const uint32_t e = pk[q] & 15u, bi = (pk[q] >> 4) & 0xFFu;
+        const size_t cell = ((size_t)q * P.E + e) * P.nb + bi;
+        const uint64_t H = P.lat[cell] < C.x_c ? Hq[cell] : 0ull;
+        const uint64_t u = tot - srv[q];
+        const uint64_t lo = H * u, hi = __umul64hi(H, u);
+        Sv = (hi << (64 - F)) | (lo >> F);
+        if (Sv < bS || bS == ~0ull) {
+          bS = Sv;
+          bq = (uint32_t)q;
+          bpk = pk[q];
+        }
+      }
+      if (a.cand) a.cand[s * M + q] = Sv;
+    }
+    const uint32_t e = bpk & 15u, bi = (bpk >> 4) & 0xFFu;
+    a.m[s] = (uint8_t)bq;
+    a.e[s] = (uint8_t)e;
+    a.B[s] = P.bs[bi];
+    a.L[s] = P.lat[((size_t)bq * P.E + e) * P.nb + bi];
+    a.S[s] = bS;
+    a.flags[s] = (bpk & 0x1000u) ? ES_FLAG_FEASIBLE : 0u;
   }
 }
 
 template <int MM>
-cudaError_t launch_block(const uint8_t *img, const ImgLayout &lay, const ScoreArgs &a, cudaStream_t st, int sms) {
-  auto kern = k1_block<MM>;
-  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lay.bytes);
+cudaError_t launch_thread(const uint8_t *img, const ImgLayout &lay, ScoreArgs a, cudaStream_t st, int sms) {
+  // the clip-path list (u32 indices) and its counter: stream-ordered scratch
+  void *scratch = nullptr;
+  const size_t list_bytes = ((size_t)a.n * sizeof(uint32_t) + 15u) & ~(size_t)15u;
+  cudaError_t e = cudaMallocAsync(&scratch, list_bytes + 16u, st);
   if (e != cudaSuccess) return e;
-  int occ = 0;
-  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, BT, lay.bytes);
-  if (e != cudaSuccess) return e;
-  if (occ < 1) return cudaErrorInvalidConfiguration;
-  int64_t blocks = a.n;
-  const int64_t cap = (int64_t)sms * occ;
-  if (blocks > cap) blocks = cap;
-  if (blocks < 1) blocks = 1;
-  kern<<<(unsigned)blocks, BT, lay.bytes, st>>>(img, lay, a);
-  return cudaGetLastError();
+  a.list = static_cast<uint32_t *>(scratch);
+  a.list_n = reinterpret_cast<unsigned long long *>(static_cast<uint8_t *>(scratch) + list_bytes);
+  e = cudaMemsetAsync(a.list_n, 0, sizeof(unsigned long long), st);
+  // one CTA of 16 warps per SM; what shared memory the staged image leaves
+  // becomes each warp's E chunk (cap positions, a multiple of 256)
+  int dev = 0, optin = 0;
+  if (e == cudaSuccess) e = cudaGetDevice(&dev);
+  if (e == cudaSuccess) e = cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+  const size_t img_b = ((size_t)a.stage_bytes + 127u) & ~(size_t)127u;
+  const int64_t room = (int64_t)optin - (int64_t)img_b - 256;
+  int64_t capw = room / K1T_WARPS;  // bytes per warp: cap * 8 + 32 + cap / 8
+  uint32_t cap = (uint32_t)std::min<int64_t>(std::max<int64_t>((capw - 32) * 8 / 65, 0) & ~255ll, 4096);
+  if (e == cudaSuccess && cap < 256u) e = cudaErrorInvalidConfiguration;
+  const size_t dyn = img_b + (size_t)K1T_WARPS * (cap * 8u + 32u + cap / 8u);
+  auto kern = k1_thread<MM>;
+  if (e == cudaSuccess) e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
+  if (e == cudaSuccess) {
+    int64_t blocks = (a.n + K1T_THREADS - 1) / K1T_THREADS;
+    if (blocks > sms) blocks = sms;
+    if (blocks < 1) blocks = 1;
+    kern<<<(unsigned)blocks, K1T_THREADS, dyn, st>>>(img, lay, a, cap);
+    e = cudaGetLastError();
+  }
+  // the listed (clip-path) snapshots: the warp-segment kernel, general path
+  if (e == cudaSuccess) e = launch_t<16, MM>(img, lay, a, st, sms);
+  const cudaError_t f = cudaFreeAsync(scratch, st);
+  return e != cudaSuccess ? e : f;
 }
 
 }  // namespace
@@ -444,16 +544,23 @@ cudaError_t launch_score(const uint8_t *img, const ImgLayout &lay, const es_snap
   a.flags = out.flags;
   a.cand = out.cand_score_q;
   a.dstat = dstat;
-  // deep snapshots (>= 1024 waits each on average): one CTA per snapshot
+  a.list = nullptr;
+  a.list_n = nullptr;
+  // many SLOs (image above 48 KB, e.g. cfg3's nine): stage only the core so
+  // that 4 CTAs fit per SM; each candidate's H is one L1-cached global load
+  a.stage_bytes = lay.bytes > 48u * 1024u ? lay.core_bytes : lay.bytes;
+  if (const char *env = getenv("ES_K1_STAGE")) a.stage_bytes = strcmp(env, "full") == 0 ? lay.bytes : lay.core_bytes;
+  // deep snapshots (>= 1024 waits each on average): the three-phase stream;
+  // Algorithm 1 on short snapshots: one thread per snapshot (clip-path ones
+  // handed to the warp segments); the baseline policies and GRID: warp segments
   const char *k1 = getenv("ES_K1");
   const bool deep = sn.n_waits > 0 && sn.n > 0 && sn.n_waits / sn.n >= 1024;
-  // the baseline policies and GRID run on the warp-segment mapping only
   const bool pol = lay.pol_mask != (1u << ES_POLICY_EDGESERVING);
   if (!pol && (k1 ? strcmp(k1, "stream") == 0 : deep)) return launch_score_stream(img, lay, sn, out, dstat, st, sms);
-  if (!pol && k1 && strcmp(k1, "block") == 0) {
-    if (lay.M <= 2) return launch_block<2>(img, lay, a, st, sms);
-    if (lay.M <= 4) return launch_block<4>(img, lay, a, st, sms);
-    return launch_block<8>(img, lay, a, st, sms);
+  if (!pol && (k1 ? strcmp(k1, "thread") == 0 : true)) {
+    if (lay.M <= 2) return launch_thread<2>(img, lay, a, st, sms);
+    if (lay.M <= 4) return launch_thread<4>(img, lay, a, st, sms);
+    return launch_thread<8>(img, lay, a, st, sms);
   }
   int lps = 16;
   if (const char *env = getenv("ES_K1_LPS")) {

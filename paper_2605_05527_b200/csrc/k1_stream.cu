@@ -7,13 +7,12 @@
 //   A  k1s_prep    one thread per queue: CSR, head wait (Q7), clipped prefix
 //                  by binary search (counted, never read), Eq. 5 / Eq. 6 of
 //                  the queue's own candidate, "can clip" flag of the snapshot
-//   B  k1s_stream_fast / k1s_stream_slow  one warp per queue, coalesced loads
-//                  in flight per lane (double-buffered on the fast path):
-//                  fast path   sum G over the live window (+ the own served
-//                              head for the candidate's exclusion)
-//                  clip path   (K_m, U_m) for every candidate m of the snapshot
-//                  read-window validation (Q24); u64 atomics into the
-//                  snapshot's accumulators
+//   B  k1s_stream_tma  fast path (snapshot cannot clip): the flat waits array
+//                  streamed through per-warp TMA rings, sum of G over every
+//                  live window (+ the own served head), Q24 check
+//      k1s_clip    clip path: one warp per clip-path snapshot, (K_m, U_m) for
+//                  every candidate m, per-wait threshold tests only near the
+//                  clip boundary and in served heads
 //   C  k1s_finish  one segment of 8 lanes per snapshot: S_q(m) for every
 //                  candidate, Eq. 7 argmin (S, m) (Q3), outputs
 // Scratch (records + accumulators) is stream-ordered (cudaMallocAsync).
@@ -90,6 +89,7 @@ __global__ void __launch_bounds__(256, 6) k1s_prep(const uint8_t *__restrict__ g
     const int k = on ? (a.cfg_idx ? (int)a.cfg_idx[s] : 0) : 0;
     QRec r{};
     uint32_t nsv = 0u;
+    bool slowq = false;
     SmemCfg C{};
     if (on && k >= P.ncfg) atomicOr(a.acc + s * ACC + 1, F_BAD);
     if (on && k < P.ncfg) {
@@ -124,9 +124,16 @@ __global__ void __launch_bounds__(256, 6) k1s_prep(const uint8_t *__restrict__ g
       r.H = r.L < C.x_c ? reinterpret_cast<const uint64_t *>(P.hb + C.off_H)[((size_t)g * P.E + e) * P.nb + bi] : 0ull;
       nsv = r.B < r.len ? r.B : r.len;
       if (wmax >= C.fast_lim || C.x_c > V4_LIM) {
+        slowq = true;
         const unsigned long long was = atomicOr(a.acc + s * ACC + 1, F_SLOW);
         if (!(was & F_SLOW)) a.slow_list[atomicAdd(a.slow_n, 1ull)] = s;
       }
+    }
+    // the clip path excludes served tasks per wait: when a snapshot's queues
+    // share this warp (M divides 32) and one of them clips, skip its served heads
+    if ((32 % M) == 0) {
+      const unsigned segm = (M == 32 ? FULL : ((1u << M) - 1u)) << ((lane / M) * M);
+      if (__ballot_sync(FULL, slowq) & segm) nsv = 0u;
     }
     // own served heads for the fast path (the clip path excludes them
     // per task): the warp reads its 32 queues' first min(B*, len) waits with
@@ -465,7 +472,7 @@ __global__ void __launch_bounds__(TMA_NW * 32, 1) k1s_stream_tma(const uint8_t *
   }
   pdl_wait();  // k1s_prep's snapshot flags
   if ((int64_t)*a.slow_n == a.n) {
-    // every snapshot takes the clip path (k1s_stream_slow reads its live
+    // every snapshot takes the clip path (k1s_clip reads their live
     // windows): nothing to stream here; drain the pieces already in flight
     for (int64_t k = 0; k < min((int64_t)rg.nsl - 1, npieces); ++k) mbar_wait(bars + 8u * (uint32_t)k, 0u);
     return;
@@ -675,78 +682,127 @@ __global__ void __launch_bounds__(TMA_NW * 32, 1) k1s_stream_tma(const uint8_t *
   flush_snap();
 }
 
-// clip path (some head wait is within max L of x_c): (K_m, U_m) for every candidate
+// clip path (some head wait is within max L of x_c): (K_m, U_m) for every
+// candidate m of the snapshot, one warp per clip-path snapshot.  Lane g < M
+// holds queue g's record; the warp walks the live windows [c_q, len_q) of the
+// snapshot's queues in rows of 32 consecutive waits (four rows' loads in
+// flight).  Waits are non-increasing from the head (checked, Q24), so a row
+// whose first wait is below every candidate's threshold min_m thr_m and which
+// lies past the queue's served head is below x_c - L_m for every m:
+// its G values go to one running sum T that every U_m receives.  Only the
+// rows near the clip boundary (w >= min thr) or in a served head compare each
+// wait with the M thresholds.  One reduce-scatter per snapshot leaves (U_m,
+// K_m) in the lanes that store them (plain stores: one writer per snapshot).
 template <int MM>
-__global__ void __launch_bounds__(256) k1s_stream_slow(const uint8_t *__restrict__ gimg, ImgLayout lay,
-                                                       StreamArgs a) {
+__device__ __forceinline__ void reduce_scatter(uint64_t (&U)[MM], uint32_t (&K)[MM], int lane) {
+  // step with offset o keeps half the remaining entries: the upper half in
+  // lanes with bit o set; afterwards entry 0 holds m = lane >> (5 - log2 MM)
+#pragma unroll
+  for (int h = MM / 2, o = 16; h >= 1; h >>= 1, o >>= 1) {
+    const bool up = (lane & o) != 0;
+#pragma unroll
+    for (int i = 0; i < h; ++i) {
+      const uint64_t su = up ? U[i] : U[i + h], ku = up ? U[i + h] : U[i];
+      const uint32_t sk = up ? K[i] : K[i + h], kk = up ? K[i + h] : K[i];
+      U[i] = ku + __shfl_xor_sync(FULL, su, o);
+      K[i] = kk + __shfl_xor_sync(FULL, sk, o);
+    }
+  }
+#pragma unroll
+  for (int o = 16 / MM; o >= 1; o >>= 1) {
+    U[0] += __shfl_xor_sync(FULL, U[0], o);
+    K[0] += __shfl_xor_sync(FULL, K[0], o);
+  }
+}
+
+template <int MM>
+__global__ void __launch_bounds__(256) k1s_clip(const uint8_t *__restrict__ gimg, ImgLayout lay, StreamArgs a) {
   pdl_trigger();
   pdl_wait();
   const int64_t n_slow = (int64_t)*a.slow_n;  // block-uniform
   if (n_slow == 0) return;
   extern __shared__ __align__(16) uint8_t smem[];
   __shared__ uint64_t mbar;
-  stage_image(smem, gimg, lay.bytes, &mbar);
+  stage_image(smem, gimg, lay.core_bytes, &mbar);  // A and Bt (H comes with the records)
   const SmemProf P = smem_prof(smem, lay);
   const int M = P.M;
   const int lane = threadIdx.x & 31;
   const int64_t wid = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  constexpr int UNR = 4;
-  for (int64_t li = wid; li < n_slow * M; li += nw) {  // warp-uniform
-    const int64_t s = a.slow_list[li / M];
-    const int g = (int)(li % M);
-    const int64_t qi = s * M + g;
-    const QRec r = a.rec[qi];
-    if (r.len <= r.c) continue;
-    unsigned long long *acc = a.acc + s * ACC;
-    const SmemCfg C = smem_cfg(P, a.cfg_idx ? (int)a.cfg_idx[s] : 0);
-    const uint32_t *W = a.waits + r.lo;
+  for (int64_t li = wid; li < n_slow; li += nw) {  // warp-uniform
+    const int64_t s = a.slow_list[li];
+    const SmemCfg C = smem_cfg(P, a.cfg_idx ? (int)a.cfg_idx[s] : 0);  // < ncfg (k1s_prep)
+    uint64_t rlo = 0;
+    uint32_t rlen = 0, rc = 0, rB = 0, rthr = 0xFFFFFFFFu;
+    if (lane < M) {
+      const QRec *r = a.rec + s * M + lane;
+      rlo = r->lo;
+      rlen = r->len;
+      rc = r->c;
+      rB = r->B;
+      if (rlen) rthr = r->thr;  // empty queue: no candidate (its sums are unused)
+    }
+    uint32_t thr[MM], K[MM];
     uint64_t U[MM];
-    uint32_t K[MM], thr[MM];
 #pragma unroll
     for (int m = 0; m < MM; ++m) {
-      U[m] = 0ull;
+      thr[m] = __shfl_sync(FULL, rthr, m);
       K[m] = 0u;
-      thr[m] = m < M ? a.rec[s * M + m].thr : 0xFFFFFFFFu;
+      U[m] = 0ull;
     }
+    const uint32_t minthr = redux_min(rthr);
+    uint64_t T = 0ull;  // G over the rows below every threshold
     bool bad = false;
-    uint32_t carry = 0xFFFFFFFFu;
-    for (uint32_t p0 = r.c; p0 < r.len; p0 += UNR * 32u) {  // warp-uniform trip count
-      uint32_t wv[UNR];
+    for (int q = 0; q < M; ++q) {  // warp-uniform
+      const uint32_t len = __shfl_sync(FULL, rlen, q), c = __shfl_sync(FULL, rc, q);
+      if (len <= c) continue;
+      const uint32_t B = __shfl_sync(FULL, rB, q);
+      const uint32_t *W = a.waits + __shfl_sync(FULL, rlo, q);
+      uint32_t carry = 0xFFFFFFFFu;  // no predecessor check at the first live wait
+      for (uint32_t p0 = c; p0 < len; p0 += 128u) {  // warp-uniform
+        uint32_t wv[4];
 #pragma unroll
-      for (int j = 0; j < UNR; ++j) {
-        const uint32_t p = p0 + j * 32u + lane;
-        wv[j] = p < r.len ? __ldg(W + p) : 0u;
-      }
+        for (int j = 0; j < 4; ++j) {
+          const uint32_t p = p0 + 32u * j + lane;
+          wv[j] = p < len ? __ldg(W + p) : 0u;
+        }
 #pragma unroll
-      for (int j = 0; j < UNR; ++j) {
-        const uint32_t p = p0 + j * 32u + lane;
-        const uint32_t w = wv[j];
-        uint32_t prev = __shfl_up_sync(FULL, w, 1);
-        if (lane == 0) prev = carry;
-        carry = __shfl_sync(FULL, w, 31);
-        if (p >= r.len) continue;
-        bad |= w > prev || w >= C.x_c;
-        const uint32_t gw = G_of(P, C, w);
+        for (int j = 0; j < 4; ++j) {
+          const uint32_t r0 = p0 + 32u * j;
+          if (r0 >= len) break;
+          const uint32_t p = r0 + lane, w = wv[j];
+          uint32_t prev = __shfl_up_sync(FULL, w, 1);
+          if (lane == 0) prev = carry;
+          carry = __shfl_sync(FULL, w, 31);
+          const uint32_t rowmax = __shfl_sync(FULL, w, 0);
+          const bool valid = p < len;
+          bad |= valid && (w > prev || w >= C.x_c);
+          if (rowmax < minthr && r0 >= B) {  // below every threshold, no served task
+            if (valid) T += G_of(P, C, w);
+            continue;
+          }
+          if (!valid) continue;
+          const uint32_t gw = G_of(P, C, w);
 #pragma unroll
-        for (int m = 0; m < MM; ++m) {
-          if (m == g && p < r.B) continue;  // candidate g's own served tasks
-          if (w >= thr[m]) K[m] += 1u;
-          else U[m] += gw;
+          for (int m = 0; m < MM; ++m) {
+            if (m == q && p < B) continue;  // candidate q's own served tasks
+            if (w >= thr[m]) K[m] += 1u;
+            else U[m] += gw;
+          }
         }
       }
     }
-    if (__any_sync(FULL, bad) && lane == 0) atomicOr(acc + 1, F_BAD);
 #pragma unroll
-    for (int m = 0; m < MM; ++m) {
-      if (m >= M) break;
-      const uint64_t u = wsum64(U[m]);
-      const uint32_t kk = redux_add(K[m]);
-      if (lane == 0) {
-        if (u) atomicAdd(acc + 2 + m, (unsigned long long)u);
-        if (kk) atomicAdd(acc + 2 + MAXM + m, (unsigned long long)kk);
-      }
+    for (int m = 0; m < MM; ++m) U[m] += T;
+    const bool anybad = __any_sync(FULL, bad);
+    reduce_scatter<MM>(U, K, lane);
+    unsigned long long *acc = a.acc + s * ACC;
+    const int m = lane >> (5 - (MM == 8 ? 3 : MM == 4 ? 2 : 1));
+    if ((lane & (32 / MM - 1)) == 0 && m < M) {
+      acc[2 + m] = U[0];
+      acc[2 + MAXM + m] = K[0];
     }
+    if (anybad && lane == 0) atomicOr(acc + 1, F_BAD);
   }
 }
 
@@ -936,9 +992,9 @@ cudaError_t launch_score_stream(const uint8_t *img, const ImgLayout &lay, const 
   if (e == cudaSuccess) e = launch_persistent(k1s_prep, img, lay, a, nq, 256, lay.bytes, st, sms, false);
   if (e == cudaSuccess) e = launch_fast(img, lay, a, nq, st, sms);
   if (e == cudaSuccess) {
-    if (lay.M <= 2) e = launch_persistent(k1s_stream_slow<2>, img, lay, a, nq, 8, lay.bytes, st, sms);
-    else if (lay.M <= 4) e = launch_persistent(k1s_stream_slow<4>, img, lay, a, nq, 8, lay.bytes, st, sms);
-    else e = launch_persistent(k1s_stream_slow<8>, img, lay, a, nq, 8, lay.bytes, st, sms);
+    if (lay.M <= 2) e = launch_persistent(k1s_clip<2>, img, lay, a, sn.n, 8, lay.core_bytes, st, sms);
+    else if (lay.M <= 4) e = launch_persistent(k1s_clip<4>, img, lay, a, sn.n, 8, lay.core_bytes, st, sms);
+    else e = launch_persistent(k1s_clip<8>, img, lay, a, sn.n, 8, lay.core_bytes, st, sms);
   }
   if (e == cudaSuccess) e = launch_persistent(k1s_finish, img, lay, a, sn.n, 32, 0, st, sms);
   const cudaError_t f = cudaFreeAsync(scratch, st);

@@ -28,7 +28,8 @@ rho = [0.60 + 0.05 * g for g in range(G)]
 cols = [0, 4, 8, 12]
 lines = [f"cfg2 synthetic (4,096 scenarios x 10k requests, tau 50 ms, M=4, E=4, B 1-16); "
          f"violation % / P95 ms per rho_full; over all loads: effective accuracy (Table I, P:500-504), "
-         f"mean exit index (0 = shallowest, {E - 1} = final) and the exit-depth histogram (% of completions, P:489)",
+         f"mean exit index (0 = shallowest, {E - 1} = final) and the exit-depth histogram (% of completions, P:489); "
+         f"every request of the finite traces completes (drain, DESIGN.md Q13): overload backlogs count in P95 and violations",
          f"{'policy':13s}" + "".join(f"   rho {rho[g]:.2f}      " for g in cols) +
          "  eff.acc  mean exit  " + " ".join(f"exit{e:d}" for e in range(E)) + "   decisions"]
 per_model = {}

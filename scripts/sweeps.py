@@ -44,7 +44,7 @@ def run(prof, cfg, weights, seed=11):
 
 hdr = f"{'':22s}" + "".join(f"   rho {r:.1f}      " for r in RHO) + "  mean exit"
 print("f3 sweeps, synthetic 3 models x 4 exits x batch 1-10 (B_max 10), 512 scenarios x 5k requests per rho;"
-      " violation % / P95 ms")
+      " violation % / P95 ms; every request of the finite traces completes (drain, DESIGN.md Q13)")
 print("\n# exit-point configuration (tau 50 ms, rates 3:2:1)")
 print(hdr)
 for name, allowed in [("layer1+final", [0, 3]), ("layer2+final", [1, 3]), ("layer3+final", [2, 3]),

@@ -150,6 +150,54 @@ def test_k1_stream_live_windows(monkeypatch, base_off):
     assert (ref["flags"][planted] & 4).all()  # every planted inversion is in the read window
 
 
+@pytest.mark.parametrize("base_off", [0, 1, 3])
+def test_k1_thread_balanced_pass(monkeypatch, base_off):
+    """The thread-per-snapshot mapping's balanced pass (one SLO per warp, the
+    region of 32 snapshots' waits cut into shared-memory chunks of `cap`
+    positions): regions far above one chunk (queues up to 60 over 8 models),
+    a waits pointer misaligned by base_off elements, empty queues, a batch
+    size that is not a multiple of 32, a few clip-path snapshots (handed to the
+    warp segments), a warp with two SLOs (the per-lane loop), and inversions
+    planted inside queues, at their last wait and at a chunk-sized stride
+    (flagged bad, Q24) -- element by element against the oracle."""
+    monkeypatch.setenv("ES_K1", "thread")
+    M = 8
+    prof = inputs.synth_profile(M, 5, list(range(1, 33)))
+    cfgs = [inputs.SchedCfg(tau=50000, b_max=32), inputs.SchedCfg(tau=90000, b_max=20)]
+    n = 32 * 23 + 7
+    q_off, w = inputs.snapshots_uniform(77, n, M, 60, 60000)
+    w = w.copy()
+    rng = np.random.default_rng(9)
+    ci = np.zeros(n, np.uint16)
+    ci[32 * 3:32 * 4] = 1          # a whole warp on the second SLO (balanced pass, its tables)
+    ci[32 * 5 + 7] = 1             # one warp with two SLOs (per-lane loop)
+    clip = rng.choice(n, 6, replace=False)
+    for s in clip:  # clip path: a head past x_c - max L
+        lo, hi = int(q_off[s * M]), int(q_off[s * M + 1])
+        if hi > lo:
+            w[lo] = 200000
+    planted = []
+    for j, s in enumerate(rng.choice(np.setdiff1d(np.arange(n), clip), 14, replace=False)):
+        m = int(rng.integers(M))
+        lo, hi = int(q_off[s * M + m]), int(q_off[s * M + m + 1])
+        if hi - lo < 3:
+            continue
+        pos = [lo + (hi - lo) // 2, hi - 1][j % 2]
+        w[pos] = w[pos - 1] + 1
+        planted.append(s)
+    h = es.es_load_profile(prof, cfgs)
+    buf = np.zeros(w.size + base_off, np.uint32)
+    buf[base_off:] = w
+    dw = to_dev(buf, torch.uint32)[base_off:]
+    o = es.es_score_candidates(h, to_dev(q_off, torch.uint64), dw, to_dev(ci, torch.uint16))
+    torch.cuda.synchronize()
+    g = {k: np_of(v) for k, v in o.items()}
+    ref = oracle.decide_batch(prof, cfgs, q_off, w, ci)
+    assert_k1_equal(g, ref, M)
+    assert (ref["flags"][planted] & 4).all()
+    assert (ref["flags"] & 4).sum() >= len(planted)
+
+
 def test_k1_masks_and_flags():
     """exit masks (ablation), no-work, bad input, bad cfg index."""
     prof = inputs.synth_profile(3, 4, [1, 2, 4, 8])
@@ -417,7 +465,7 @@ def test_k2_segment_widths(monkeypatch, lps):
     test_k2_errors()
 
 
-@pytest.mark.parametrize("mode", ["stream", "block", "seg"])
+@pytest.mark.parametrize("mode", ["stream", "thread", "seg"])
 def test_k1_all_mappings(monkeypatch, mode):
     """K1's mappings (3-phase streaming and one CTA per snapshot for deep
     queues, warp segments for small ones) on every K1 input family."""
