@@ -158,6 +158,8 @@ es_status es_load_profile(const es_profile_desc *desc, const es_sched_cfg *cfgs,
   uint32_t off = 0;
   lay.off_lat = off;
   off = align16(off + 4u * cells);
+  lay.off_latT = off;
+  off = align16(off + 32u * M * nb);
   lay.off_bs = off;
   off = align16(off + 2u * nb);
   lay.off_mask = off;
@@ -213,6 +215,12 @@ es_status es_load_profile(const es_profile_desc *desc, const es_sched_cfg *cfgs,
 
   std::vector<uint8_t> img(lay.bytes, 0);
   memcpy(img.data() + lay.off_lat, desc->latency_us, 4u * cells);
+  for (int m = 0; m < M; ++m)
+    for (int b = 0; b < nb; ++b)
+      for (int e = 0; e < 8; ++e) {
+        const uint32_t v = e < E ? desc->latency_us[(m * E + e) * nb + b] : 0xFFFFFFFFu;
+        memcpy(img.data() + lay.off_latT + 4u * ((m * nb + b) * 8 + e), &v, 4);
+      }
   for (int b = 0; b < nb; ++b) {
     const uint16_t v = (uint16_t)desc->batch_sizes[b];
     memcpy(img.data() + lay.off_bs + 2 * b, &v, 2);

@@ -52,6 +52,7 @@ struct SmemProf {
   const uint8_t *sm;
   const uint8_t *hb;  // base of the H tables: the staged image, or the global one (core-only staging)
   const uint32_t *lat;
+  const uint32_t *latT;  // [M][nb][8], exit-minor, padded (Eq. 6 by counting)
   const uint16_t *bs;
   const uint32_t *mask;
   const uint16_t *acc;  // [M][E] accuracy, basis points
@@ -64,6 +65,7 @@ __device__ __forceinline__ SmemProf smem_prof(const uint8_t *sm, const ImgLayout
   p.sm = sm;
   p.hb = sm;
   p.lat = reinterpret_cast<const uint32_t *>(sm + lay.off_lat);
+  p.latT = reinterpret_cast<const uint32_t *>(sm + lay.off_latT);
   p.bs = reinterpret_cast<const uint16_t *>(sm + lay.off_bs);
   p.mask = reinterpret_cast<const uint32_t *>(sm + lay.off_mask);
   p.acc = reinterpret_cast<const uint16_t *>(sm + lay.off_acc);
@@ -248,6 +250,20 @@ struct Seg {
   }
 };
 
+// Eq. 6 as a count: the number of exits e with L(m, e, bs[bi]) <=
+// lim, i.e. the length of the feasible prefix (L strictly increasing in e;
+// the padding 0xFFFFFFFF never counts).  lim < 2^32 - 1.
+__device__ __forceinline__ uint32_t eq6_count(const SmemProf &P, int m, uint32_t bi, uint32_t lim) {
+  const uint4 *row = reinterpret_cast<const uint4 *>(P.latT + ((size_t)m * P.nb + bi) * 8u);
+  const uint4 x = row[0];
+  uint32_t c = (x.x <= lim) + (x.y <= lim) + (x.z <= lim) + (x.w <= lim);
+  if (P.E > 4) {
+    const uint4 y = row[1];
+    c += (y.x <= lim) + (y.y <= lim) + (y.z <= lim) + (y.w <= lim);
+  }
+  return c;
+}
+
 // per-group candidate (uniform across the group's lanes)
 struct Cand {
   uint32_t B, e, L, thr;
@@ -295,17 +311,10 @@ __device__ __forceinline__ Cand cand_params(const Seg<LPS, MM> &sg, const SmemPr
   }
   // more exits than group lanes: every lane evaluates Eq. 6 for its group's
   // model itself.  L is strictly increasing in e (validated), so the exits
-  // with wmax + L <= tau are the first c ones: c by a 4-step binary search
-  // (E <= 8), then the mask keeps the allowed ones.
-  if (wmax <= C.tau) {
-    const uint32_t lim = C.tau - wmax;  // wmax + L <= tau  <=>  L <= lim
-    uint32_t c = 0u;  // binary lifting: c < 16 covers E <= 8
-    if (8 <= P.E && row[7 * P.nb] <= lim) c = 8u;
-    if (c + 4u <= (uint32_t)P.E && row[(c + 3u) * P.nb] <= lim) c += 4u;
-    if (c + 2u <= (uint32_t)P.E && row[(c + 1u) * P.nb] <= lim) c += 2u;
-    if (c + 1u <= (uint32_t)P.E && row[c * P.nb] <= lim) c += 1u;
-    bits = ((1u << c) - 1u) & mbits;
-  }
+  // with wmax + L <= tau are the first c ones: c counted on the padded
+  // exit-minor row (two independent 16-byte loads), then the mask keeps the
+  // allowed ones.
+  if (wmax <= C.tau) bits = ((1u << eq6_count(P, gg, bi, C.tau - wmax)) - 1u) & mbits;
   k.feas = bits != 0u;
   k.e = k.feas ? 31u - __clz(bits) : (uint32_t)(__ffs(mbits) - 1);
   if (fixed) k.e = fixed == 1 ? 31u - __clz(mbits) : (uint32_t)(__ffs(mbits) - 1);

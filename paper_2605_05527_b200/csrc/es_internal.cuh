@@ -4,6 +4,8 @@
 // memory that every kernel stages into shared memory with a single TMA bulk
 // copy (cp.async.bulk + mbarrier).  Layout (byte offsets in ImgLayout):
 //   lat   u32 [M][E][nb]    L(m, e, bs[b]) in us
+//   latT  u32 [M][nb][8]    the same, exit-minor, padded with 0xFFFFFFFF (one
+//                           16-byte row pair per (m, b): Eq. 6 as a count)
 //   bs    u16 [nb]          profiled batch sizes
 //   mask  u32 [M]           allowed-exit bitmask per model  (P:517-527 ablation)
 //   acc   u16 [M][E]        top-1 accuracy per (model, exit), basis points (Table I)
@@ -40,6 +42,7 @@ struct ImgLayout {
   uint32_t core_bytes;  // prefix without the per-cfg H tables (they form the tail)
   int32_t M, E, nb, ncfg;
   uint32_t off_lat, off_bs, off_mask, off_acc, off_cfg;
+  uint32_t off_latT;  // latT u32 [M][nb][8]: L(m, e, bs[b]) for e < E, 0xFFFFFFFF past E (Eq. 6 by counting)
   // cfg 0's urgency-table constants (host-computed), kernel parameters for the
   // single-SLO specialisation of the K1 stream: byte offsets of A and Bt, 4 r,
   // and the A index mask 4 (2^k - 1) with 2^k >= nA_cap

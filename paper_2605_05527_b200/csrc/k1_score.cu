@@ -170,8 +170,8 @@ cudaError_t launch_lps(const uint8_t *img, const ImgLayout &lay, const ScoreArgs
 // A warp segment spends warp-wide shuffles and reductions on a handful of
 // waits (harvested cfg3 states: 33 waits over 8 queues on average, median
 // queue 2), so here each lane owns a snapshot's decision logic:
-//   per queue q: Eq. 5 (bidx, Q8) and Eq. 6 (binary search on the strictly
-//   increasing exit latencies, Q2); S_q(m) = floor(H(L_m) (tot - srv_m) /
+//   per queue q: Eq. 5 (bidx, Q8) and Eq. 6 (a count over the padded
+//   exit-minor latency row, Q2); S_q(m) = floor(H(L_m) (tot - srv_m) /
 //   2^28) and the Eq. 7 argmin (S, m) (Q3) -- the fast path of decide.cuh
 //   (same integers), valid when every head wait is below x_c - max L.
 // The sums come from one balanced pass of the whole warp: the waits of the
@@ -237,14 +237,24 @@ __global__ void __launch_bounds__(K1T_THREADS, 1) k1_thread(const uint8_t *__res
     if (a.cand)
       for (int q = 0; q < M; ++q) a.cand[s * M + q] = ~0ull;
   };
-  // each warp takes one contiguous block of snapshots, 32 per iteration: the
-  // next iteration's CSR rows, SLO indices and waits follow this one's, so
-  // they are prefetched into L2 while this one is scored
-  const int64_t per = ((a.n + nwarps - 1) / nwarps + 31) & ~31ll;
-  const int64_t wbeg = ((int64_t)blockIdx.x * K1T_WARPS + wib) * per, wend = min(wbeg + per, a.n);
-  for (int64_t s0 = wbeg; s0 < wend; s0 += 32) {  // warp-uniform
+  // warps stride over groups of 32 snapshots (snapshot sizes are correlated
+  // along the batch: strided groups balance the warps); the next group's CSR
+  // rows and SLO indices are prefetched into L2 at the start of a group, its
+  // waits region once its bounds (loaded early) are known
+  const int64_t stride = nwarps * 32;
+  const int64_t wend = a.n;
+  for (int64_t s0 = ((int64_t)blockIdx.x * K1T_WARPS + wib) * 32; s0 < a.n; s0 += stride) {  // warp-uniform
     const int64_t s = s0 + lane;
     const bool live = s < wend;
+    const int64_t s1 = s0 + stride;  // the next group
+    uint64_t nb = 0ull;  // lane 0: its region start, lane 31: its region end
+    if (s1 < a.n) {
+      const char *nq = reinterpret_cast<const char *>(a.q_off + s1 * M);
+      if ((uint32_t)lane * 128u < 32u * 8u * (uint32_t)M + 8u) asm volatile("prefetch.global.L2 [%0];" ::"l"(nq + 128 * lane));
+      if (lane == 30 && a.cfg_idx) asm volatile("prefetch.global.L2 [%0];" ::"l"(a.cfg_idx + s1));
+      if (lane == 0) nb = __ldg(a.q_off + s1 * M);
+      if (lane == 31) nb = __ldg(a.q_off + min(s1 + 32, a.n) * M);
+    }
     const int k = live ? (a.cfg_idx ? (int)a.cfg_idx[s] : 0) : 0;
     const bool cfg_ok = k < P.ncfg;
     const SmemCfg C = smem_cfg(P, cfg_ok ? k : 0);
@@ -259,13 +269,10 @@ __global__ void __launch_bounds__(K1T_THREADS, 1) k1_thread(const uint8_t *__res
 #pragma unroll
     for (int q = 0; q <= MM; ++q)
       if (q == M) R1 = __shfl_sync(FULL, off[q], ll);
-    if (s0 + 32 < wend) {  // L2 prefetch of the next iteration: CSR rows, SLO indices, first 8 KB of waits
-      const char *nq = reinterpret_cast<const char *>(a.q_off + (s0 + 32) * M);
-      if ((uint32_t)lane * 128u < 32u * 8u * (uint32_t)M + 8u) asm volatile("prefetch.global.L2 [%0];" ::"l"(nq + 128 * lane));
-      if (lane == 31 && a.cfg_idx) asm volatile("prefetch.global.L2 [%0];" ::"l"(a.cfg_idx + s0 + 32));
-      const char *nw = reinterpret_cast<const char *>(a.waits + R1);
-      asm volatile("prefetch.global.L2 [%0];" ::"l"(nw + 128 * lane));
-      asm volatile("prefetch.global.L2 [%0];" ::"l"(nw + 128 * (lane + 32)));
+    {  // L2 prefetch of the next group's waits region (its bounds loaded at the top)
+      const uint64_t n0 = __shfl_sync(FULL, nb, 0), n1 = __shfl_sync(FULL, nb, 31);
+      const char *nw = reinterpret_cast<const char *>(a.waits + n0);
+      for (uint64_t b = 128u * (uint64_t)lane; b < 4u * (n1 - n0); b += 4096u) asm volatile("prefetch.global.L2 [%0];" ::"l"(nw + b));
     }
     uint32_t head[MM];
     bool slow = false, any = false;
@@ -302,18 +309,8 @@ __global__ void __launch_bounds__(K1T_THREADS, 1) k1_thread(const uint8_t *__res
       const uint32_t cap_b = len < C.b_max ? len : C.b_max;
       const uint32_t bi = P.sm[C.off_bidx + cap_b];
       nsv[q] = min((uint32_t)P.bs[bi], len);
-      const uint32_t *row = P.lat + (size_t)q * P.E * P.nb + bi;  // row[e * nb]
       const uint32_t mbits = P.mask[q];
-      unsigned bits = 0u;
-      if (head[q] <= C.tau) {
-        const uint32_t lim = C.tau - head[q];
-        uint32_t c = 0u;
-        if (8 <= P.E && row[7 * P.nb] <= lim) c = 8u;
-        if (c + 4u <= (uint32_t)P.E && row[(c + 3u) * P.nb] <= lim) c += 4u;
-        if (c + 2u <= (uint32_t)P.E && row[(c + 1u) * P.nb] <= lim) c += 2u;
-        if (c + 1u <= (uint32_t)P.E && row[c * P.nb] <= lim) c += 1u;
-        bits = ((1u << c) - 1u) & mbits;
-      }
+      const unsigned bits = head[q] <= C.tau ? ((1u << eq6_count(P, q, bi, C.tau - head[q])) - 1u) & mbits : 0u;
       const uint32_t e = bits ? 31u - __clz(bits) : (uint32_t)(__ffs(mbits) - 1);
       pk[q] = e | (bi << 4) | (bits ? 0x1000u : 0u);
     }
@@ -468,8 +465,8 @@ __global__ void __launch_bounds__(K1T_THREADS, 1) k1_thread(const uint8_t *__res
       uint64_t Sv = ~0ull;
       if (pk[q] != 0xFFFFFFFFu) {
         const uint32_t e = pk[q] & 15u, bi = (pk[q] >> 4) & 0xFFu;
-        const size_t cell = ((size_t)q * P.E + e) * P.nb + bi;
-        const uint64_t H = P.lat[cell] < C.x_c ? Hq[cell] : 0ull;
+        const uint64_t Hc = Hq[((size_t)q * P.E + e) * P.nb + bi];
+        const uint64_t H = Hc == ~0ull ? 0ull : Hc;  // L >= x_c: every task clips (k_build_tables)
         const uint64_t u = tot - srv[q];
         const uint64_t lo = H * u, hi = __umul64hi(H, u);
         Sv = (hi << (64 - F)) | (lo >> F);
@@ -485,7 +482,7 @@ __global__ void __launch_bounds__(K1T_THREADS, 1) k1_thread(const uint8_t *__res
     a.m[s] = (uint8_t)bq;
     a.e[s] = (uint8_t)e;
     a.B[s] = P.bs[bi];
-    a.L[s] = P.lat[((size_t)bq * P.E + e) * P.nb + bi];
+    a.L[s] = P.latT[((size_t)bq * P.nb + bi) * 8u + e];
     a.S[s] = bS;
     a.flags[s] = (bpk & 0x1000u) ? ES_FLAG_FEASIBLE : 0u;
   }

@@ -685,8 +685,8 @@ __global__ void __launch_bounds__(TMA_NW * 32, 1) k1s_stream_tma(const uint8_t *
 // clip path (some head wait is within max L of x_c): (K_m, U_m) for every
 // candidate m of the snapshot, one warp per clip-path snapshot.  Lane g < M
 // holds queue g's record; the warp walks the live windows [c_q, len_q) of the
-// snapshot's queues in rows of 32 consecutive waits (four rows' loads in
-// flight).  Waits are non-increasing from the head (checked, Q24), so a row
+// snapshot's queues in rows of 32 consecutive waits (eight rows' loads in
+// flight; the next snapshot's windows prefetched into L2).  Waits are non-increasing from the head (checked, Q24), so a row
 // whose first wait is below every candidate's threshold min_m thr_m and which
 // lies past the queue's served head is below x_c - L_m for every m:
 // its G values go to one running sum T that every U_m receives.  Only the
@@ -715,6 +715,8 @@ __device__ __forceinline__ void reduce_scatter(uint64_t (&U)[MM], uint32_t (&K)[
   }
 }
 
+constexpr int CLIP_ROWS = 8;  // rows of 32 waits in flight per warp
+
 template <int MM>
 __global__ void __launch_bounds__(256) k1s_clip(const uint8_t *__restrict__ gimg, ImgLayout lay, StreamArgs a) {
   pdl_trigger();
@@ -729,6 +731,16 @@ __global__ void __launch_bounds__(256) k1s_clip(const uint8_t *__restrict__ gimg
   const int lane = threadIdx.x & 31;
   const int64_t wid = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  // the live windows of the warp's next snapshot are prefetched into L2 while
+  // this one is scored (the loop is latency-bound: one snapshot at a time)
+  auto prefetch_snap = [&](int64_t li) {
+    if (li >= n_slow || lane >= M) return;
+    const QRec *r = a.rec + a.slow_list[li] * M + lane;
+    const uint32_t len = r->len, c = r->c;
+    const char *p0 = reinterpret_cast<const char *>(a.waits + r->lo + c);
+    for (uint32_t b = 0; b < 4u * (len > c ? len - c : 0u); b += 128u) asm volatile("prefetch.global.L2 [%0];" ::"l"(p0 + b));
+  };
+  prefetch_snap(wid);
   for (int64_t li = wid; li < n_slow; li += nw) {  // warp-uniform
     const int64_t s = a.slow_list[li];
     const SmemCfg C = smem_cfg(P, a.cfg_idx ? (int)a.cfg_idx[s] : 0);  // < ncfg (k1s_prep)
@@ -742,6 +754,7 @@ __global__ void __launch_bounds__(256) k1s_clip(const uint8_t *__restrict__ gimg
       rB = r->B;
       if (rlen) rthr = r->thr;  // empty queue: no candidate (its sums are unused)
     }
+    prefetch_snap(li + nw);
     uint32_t thr[MM], K[MM];
     uint64_t U[MM];
 #pragma unroll
@@ -759,15 +772,15 @@ __global__ void __launch_bounds__(256) k1s_clip(const uint8_t *__restrict__ gimg
       const uint32_t B = __shfl_sync(FULL, rB, q);
       const uint32_t *W = a.waits + __shfl_sync(FULL, rlo, q);
       uint32_t carry = 0xFFFFFFFFu;  // no predecessor check at the first live wait
-      for (uint32_t p0 = c; p0 < len; p0 += 128u) {  // warp-uniform
-        uint32_t wv[4];
+      for (uint32_t p0 = c; p0 < len; p0 += 32u * CLIP_ROWS) {  // warp-uniform
+        uint32_t wv[CLIP_ROWS];
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
+        for (int j = 0; j < CLIP_ROWS; ++j) {
           const uint32_t p = p0 + 32u * j + lane;
           wv[j] = p < len ? __ldg(W + p) : 0u;
         }
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
+        for (int j = 0; j < CLIP_ROWS; ++j) {
           const uint32_t r0 = p0 + 32u * j;
           if (r0 >= len) break;
           const uint32_t p = r0 + lane, w = wv[j];
