@@ -190,18 +190,23 @@ cudaError_t launch_lps(const uint8_t *img, const ImgLayout &lay, const ScoreArgs
 constexpr int K1T_THREADS = 512;
 constexpr int K1T_WARPS = K1T_THREADS / 32;
 
-__device__ __forceinline__ uint32_t lds32(uint32_t a) {
+__device__ __forceinline__ uint32_t lds32(uint32_t a) {  // read-only tables / bitmap after a __syncwarp
   uint32_t v;
-  asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(a));
+  asm("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(a) : "memory");
   return v;
+}
+__device__ __forceinline__ uint32_t lds32_ro(uint32_t a) {  // staged profile tables (never written after staging)
+  uint32_t v;
+  asm("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ void sts64(uint32_t a, uint64_t x) {
+  asm volatile("st.shared.u64 [%0], %1;" ::"r"(a), "l"(x) : "memory");
 }
 __device__ __forceinline__ uint64_t lds64(uint32_t a) {
   uint64_t v;
   asm volatile("ld.shared.u64 %0, [%1];" : "=l"(v) : "r"(a));
   return v;
-}
-__device__ __forceinline__ void sts128(uint32_t a, uint64_t x, uint64_t y) {
-  asm volatile("st.shared.v2.u64 [%0], {%1, %2};" ::"r"(a), "l"(x), "l"(y) : "memory");
 }
 
 // G(w) with 32-bit shared addresses: v4 = 4 (w + r) (exact: x_c + 1024 < 2^30
@@ -212,7 +217,7 @@ struct GSh {
   __device__ __forceinline__ uint32_t operator()(uint32_t w) const {
     const uint32_t v4 = w * 4u + r4;
     const uint32_t h = min(v4 >> (SBITS + 2), nA1);
-    return (uint32_t)(((uint64_t)lds32(sA + 4u * h) * (uint64_t)lds32(sBt + (v4 & (4u * S - 4u)))) >> F);
+    return (uint32_t)(((uint64_t)lds32_ro(sA + 4u * h) * (uint64_t)lds32_ro(sBt + (v4 & (4u * S - 4u)))) >> F);
   }
 };
 
@@ -371,24 +376,27 @@ __global__ void __launch_bounds__(K1T_THREADS, 1) k1_thread(const uint8_t *__res
 #pragma unroll
           for (int i = 1; i < 8; ++i) gt |= w[i] > w[i - 1] ? 1u << i : 0u;
           inv |= (gt & vm & ~sb8) != 0u;
-          uint64_t c[8];
+          // G of every loaded wait (masked positions hold 0: G(0) is in range)
+          uint32_t g[8];
+          uint64_t ls = 0ull;
 #pragma unroll
           for (int i = 0; i < 8; ++i) {
-            const uint64_t g = (vm >> i) & 1u ? (uint64_t)G(w[i]) : 0ull;
-            c[i] = i ? c[i - 1] + g : g;
+            g[i] = G(w[i]) & (0u - ((vm >> i) & 1u));
+            ls += g[i];
           }
-          uint64_t sc = c[7];  // warp inclusive scan of the lane sums
+          uint64_t sc = ls;  // warp inclusive scan of the lane sums
 #pragma unroll
           for (int o = 1; o < 32; o <<= 1) {
             const uint64_t t = __shfl_up_sync(FULL, sc, o);
             if (lane >= o) sc += t;
           }
-          const uint64_t base = carry + sc - c[7];  // E at position p
+          uint64_t e = carry + sc - ls;  // E at position p
           const uint32_t ea = sE + 8u * (p - cb);
-          sts128(ea, base, base + c[0]);
-          sts128(ea + 16u, base + c[1], base + c[2]);
-          sts128(ea + 32u, base + c[3], base + c[4]);
-          sts128(ea + 48u, base + c[5], base + c[6]);
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            sts64(ea + 8u * i, e);
+            e += g[i];
+          }
           carry += __shfl_sync(FULL, sc, 31);
         }
         __syncwarp();

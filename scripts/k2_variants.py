@@ -17,7 +17,10 @@ w = inputs.workload(wl, scen_ids=np.arange(n))
 dtr = engine.upload_traces(w.traces, "cuda")
 print(f"{wl} {n} scenarios generated in {time.time() - t0:.0f} s", flush=True)
 ref = None
-for v in sys.argv[1:] or ["default"]:
+for spec in sys.argv[1:] or ["default"]:
+    v, _, envs = spec.partition("+")
+    for kv in filter(None, envs.split(",")):
+        os.environ[kv.split("=")[0]] = kv.split("=")[1]
     es._lib = None
     es.LIB_PATH = os.path.join(ROOT, "paper_2605_05527_b200", "libedgeserve.so") if v == "default" else os.path.abspath(v)
     h = es.es_load_profile(w.profile, w.cfgs)
@@ -36,5 +39,7 @@ for v in sys.argv[1:] or ["default"]:
     if ref is None:
         ref = st
     dec = float(st[:, 0].sum())
-    print(f"{os.path.basename(v):24s} K2 {np.mean(ms[1:]):8.3f} ms  {dec / np.mean(ms[1:]) * 1e3:.3e} decisions/s  {same}",
+    for kv in filter(None, envs.split(",")):
+        os.environ.pop(kv.split("=")[0])
+    print(f"{os.path.basename(spec):24s} K2 {np.mean(ms[1:]):8.3f} ms  {dec / np.mean(ms[1:]) * 1e3:.3e} decisions/s  {same}",
           flush=True)

@@ -31,7 +31,8 @@ with open(os.path.join(P, f"{R}_launches.txt"), "w") as f:
         f.write(f"{k[:60]:60s} {cnt[k]:8d} {v:12.0f} {100 * v / allns:6.1f}%\n")
 
 traffic = {}
-for tag, kern in [("k2", "k2_replay"), ("k3", "k3_stats"), ("k1", "k1_call")]:
+for tag, kern in [("k2", "k2_replay"), ("k3", "k3_stats"), ("k1", "k1_call"), ("k1h", "k1_harvested"),
+                  ("k1clip", "k1_clip")]:
     rep = os.path.join(G, f"prof_{tag}_{R}.ncu-rep")
     if not os.path.exists(rep):
         continue
