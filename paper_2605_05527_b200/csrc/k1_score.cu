@@ -263,71 +263,82 @@ __global__ void __launch_bounds__(K1T_THREADS, 1) k1_thread(const uint8_t *__res
     const int k = live ? (a.cfg_idx ? (int)a.cfg_idx[s] : 0) : 0;
     const bool cfg_ok = k < P.ncfg;
     const SmemCfg C = smem_cfg(P, cfg_ok ? k : 0);
-    // CSR row and head waits: all loads independent
-    uint64_t off[MM + 1];
+    // CSR row and head waits: all loads independent; offsets kept relative to
+    // the group's region start R0 (a region of 2^31 waits or more -- 8 GB for
+    // 32 snapshots -- goes to the warp segments whole)
+    uint32_t rel[MM + 1];
+    uint64_t R0, R1;
+    bool huge;
+    {
+      uint64_t off[MM + 1];
 #pragma unroll
-    for (int q = 0; q <= MM; ++q) off[q] = live && q <= M ? __ldg(a.q_off + s * M + q) : 0ull;
-    // the region of this iteration's waits [R0, R1): contiguous (consecutive snapshots)
-    const uint64_t R0 = __shfl_sync(FULL, off[0], 0);
-    const int ll = 31 - __clz(__ballot_sync(FULL, live));
-    uint64_t R1 = 0ull;
+      for (int q = 0; q <= MM; ++q) off[q] = live && q <= M ? __ldg(a.q_off + s * M + q) : 0ull;
+      R0 = __shfl_sync(FULL, off[0], 0);
+      const int ll = 31 - __clz(__ballot_sync(FULL, live));
+      R1 = 0ull;
 #pragma unroll
-    for (int q = 0; q <= MM; ++q)
-      if (q == M) R1 = __shfl_sync(FULL, off[q], ll);
+      for (int q = 0; q <= MM; ++q)
+        if (q == M) R1 = __shfl_sync(FULL, off[q], ll);
+      huge = R1 - R0 >= (1ull << 31);
+#pragma unroll
+      for (int q = 0; q <= MM; ++q) rel[q] = live ? (uint32_t)(off[q] - R0) : 0u;
+    }
     {  // L2 prefetch of the next group's waits region (its bounds loaded at the top)
       const uint64_t n0 = __shfl_sync(FULL, nb, 0), n1 = __shfl_sync(FULL, nb, 31);
       const char *nw = reinterpret_cast<const char *>(a.waits + n0);
       for (uint64_t b = 128u * (uint64_t)lane; b < 4u * (n1 - n0); b += 4096u) asm volatile("prefetch.global.L2 [%0];" ::"l"(nw + b));
     }
-    uint32_t head[MM];
-    bool slow = false, any = false;
-#pragma unroll
-    for (int q = 0; q < MM; ++q) {
-      const bool has = q < M && off[q + 1] > off[q];
-      head[q] = has ? __ldg(a.waits + off[q]) : 0u;
-      slow |= has && head[q] >= C.fast_lim;
-      any |= has;
-    }
+    const uint32_t *Wr = a.waits + R0;  // the region's waits
+    uint32_t pk[MM];  // e | bi << 4 | feasible << 12 | min(B*, len) << 16; 0xFFFFFFFF: empty queue
     bool active = false;
-    if (live) {
-      if (!cfg_ok) {
-        out_empty(s, ES_FLAG_BAD_INPUT);
-        if (atomicCAS(&a.dstat->code, 0u, (uint32_t)ES_ERR_ARG) == 0u) a.dstat->item = s;
-      } else if (slow) {  // some task may clip: the general path (k1_score on the list)
-        a.list[atomicAdd(a.list_n, 1ull)] = (uint32_t)s;
-      } else if (!any) {
-        out_empty(s, ES_FLAG_NO_WORK);
-      } else {
-        active = true;
+    {
+      uint32_t head[MM];
+      bool slow = false, any = false;
+#pragma unroll
+      for (int q = 0; q < MM; ++q) {
+        const bool has = q < M && rel[q + 1] > rel[q];
+        head[q] = has ? __ldg(Wr + rel[q]) : 0u;
+        slow |= has && head[q] >= C.fast_lim;
+        any |= has;
+      }
+      if (live) {
+        if (!cfg_ok) {
+          out_empty(s, ES_FLAG_BAD_INPUT);
+          if (atomicCAS(&a.dstat->code, 0u, (uint32_t)ES_ERR_ARG) == 0u) a.dstat->item = s;
+        } else if (slow || huge) {  // some task may clip: the general path (k1_score on the list)
+          a.list[atomicAdd(a.list_n, 1ull)] = (uint32_t)s;
+        } else if (!any) {
+          out_empty(s, ES_FLAG_NO_WORK);
+        } else {
+          active = true;
+        }
+      }
+      // Eq. 5 / Eq. 6 of every queue
+#pragma unroll
+      for (int q = 0; q < MM; ++q) {
+        pk[q] = 0xFFFFFFFFu;
+        const uint32_t len = q < M ? rel[q + 1] - rel[q] : 0u;
+        if (!active || !len) continue;
+        const uint32_t cap_b = len < C.b_max ? len : C.b_max;
+        const uint32_t bi = P.sm[C.off_bidx + cap_b];
+        const uint32_t nsv = min((uint32_t)P.bs[bi], len);
+        const uint32_t mbits = P.mask[q];
+        const unsigned bits = head[q] <= C.tau ? ((1u << eq6_count(P, q, bi, C.tau - head[q])) - 1u) & mbits : 0u;
+        const uint32_t e = bits ? 31u - __clz(bits) : (uint32_t)(__ffs(mbits) - 1);
+        pk[q] = e | (bi << 4) | (bits ? 0x1000u : 0u) | (nsv << 16);
       }
     }
     const unsigned b_act = __ballot_sync(FULL, active);
     if (b_act == 0u) continue;
-    // Eq. 5 / Eq. 6 of every queue (empty: 0xFFFFFFFF); nsv = min(B*, len)
-    uint32_t pk[MM], nsv[MM];  // pk = e | bi << 4 | feasible << 12
-#pragma unroll
-    for (int q = 0; q < MM; ++q) {
-      pk[q] = 0xFFFFFFFFu;
-      nsv[q] = 0u;
-      const uint32_t len = q < M ? (uint32_t)(off[q + 1] - off[q]) : 0u;
-      if (!active || !len) continue;
-      const uint32_t cap_b = len < C.b_max ? len : C.b_max;
-      const uint32_t bi = P.sm[C.off_bidx + cap_b];
-      nsv[q] = min((uint32_t)P.bs[bi], len);
-      const uint32_t mbits = P.mask[q];
-      const unsigned bits = head[q] <= C.tau ? ((1u << eq6_count(P, q, bi, C.tau - head[q])) - 1u) & mbits : 0u;
-      const uint32_t e = bits ? 31u - __clz(bits) : (uint32_t)(__ffs(mbits) - 1);
-      pk[q] = e | (bi << 4) | (bits ? 0x1000u : 0u);
-    }
     uint64_t tot = 0ull, srv[MM];
 #pragma unroll
     for (int q = 0; q < MM; ++q) srv[q] = 0ull;
     bool bad = false;
     // ---- the balanced pass: one SLO across the warp's active snapshots
     const int kf = __shfl_sync(FULL, k, __ffs(b_act) - 1);
-    const uintptr_t a0 = reinterpret_cast<uintptr_t>(a.waits + R0);
+    const uintptr_t a0 = reinterpret_cast<uintptr_t>(Wr);
     const uint32_t mis = (uint32_t)((a0 & 15u) >> 2);  // waits before R0 in its 16-byte vector
-    bool flat = __all_sync(FULL, !active || k == kf) && R1 - R0 < (1ull << 30);
+    bool flat = __all_sync(FULL, !active || k == kf);
     if (flat) {
       const uint32_t *abase = reinterpret_cast<const uint32_t *>(a0 & ~(uintptr_t)15u);  // relative position 0
       const uint32_t nrel = (uint32_t)(R1 - R0) + mis;
@@ -343,7 +354,7 @@ __global__ void __launch_bounds__(K1T_THREADS, 1) k1_thread(const uint8_t *__res
         if (live) {  // queue starts of this chunk (no predecessor check there, Q24)
 #pragma unroll
           for (int q = 0; q < MM; ++q) {
-            const uint32_t x = (uint32_t)(off[q] - R0) + mis;
+            const uint32_t x = rel[q] + mis;
             if (q < M && x >= cb && x < ce)
               asm volatile("red.shared.or.b32 [%0], %1;" ::"r"(sBits + 4u * ((x - cb) >> 5)), "r"(1u << ((x - cb) & 31u)));
           }
@@ -404,7 +415,7 @@ __global__ void __launch_bounds__(K1T_THREADS, 1) k1_thread(const uint8_t *__res
 #pragma unroll
           for (int q = 0; q <= MM; ++q) {
             if (q > M) continue;
-            const uint32_t x = (uint32_t)(off[q] - R0) + mis;
+            const uint32_t x = rel[q] + mis;
             if (x >= cb && x < ce) {
               const uint64_t e = lds64(sE + 8u * (x - cb));
               if (q == 0) tot -= e;
@@ -412,7 +423,7 @@ __global__ void __launch_bounds__(K1T_THREADS, 1) k1_thread(const uint8_t *__res
               if (q < M) srv[q] -= e;
             }
             if (q < M) {
-              const uint32_t x1 = x + nsv[q];
+              const uint32_t x1 = x + (pk[q] >> 16);
               if (x1 >= cb && x1 < ce) srv[q] += lds64(sE + 8u * (x1 - cb));
             }
           }
@@ -423,13 +434,13 @@ __global__ void __launch_bounds__(K1T_THREADS, 1) k1_thread(const uint8_t *__res
 #pragma unroll
         for (int q = 0; q <= MM; ++q) {
           if (q > M) continue;
-          const uint32_t x = (uint32_t)(off[q] - R0) + mis;
+          const uint32_t x = rel[q] + mis;
           if (x == nrel) {
             if (q == 0) tot -= carry;
             if (q == M) tot += carry;
             if (q < M) srv[q] -= carry;
           }
-          if (q < M && x + nsv[q] == nrel) srv[q] += carry;
+          if (q < M && x + (pk[q] >> 16) == nrel) srv[q] += carry;
         }
       }
       flat = !__any_sync(FULL, inv);  // an inversion: redo the warp per lane (flags it exactly)
@@ -441,10 +452,10 @@ __global__ void __launch_bounds__(K1T_THREADS, 1) k1_thread(const uint8_t *__res
 #pragma unroll
       for (int q = 0; q < MM; ++q) {
         srv[q] = 0ull;
-        const uint32_t len = q < M ? (uint32_t)(off[q + 1] - off[q]) : 0u;
+        const uint32_t len = q < M ? rel[q + 1] - rel[q] : 0u;
         if (!len) continue;
-        const uint32_t *W = a.waits + off[q];
-        uint32_t prev = head[q];
+        const uint32_t *W = Wr + rel[q];
+        uint32_t prev = __ldg(W);
         uint64_t Q = G(prev), sv = Q;  // nsv >= 1
         for (uint32_t p = 1; p < len; ++p) {
           const uint32_t w = __ldg(W + p);
@@ -452,7 +463,7 @@ __global__ void __launch_bounds__(K1T_THREADS, 1) k1_thread(const uint8_t *__res
           prev = w;
           const uint64_t g = G(w);
           Q += g;
-          if (p < nsv[q]) sv += g;
+          if (p < (pk[q] >> 16)) sv += g;
         }
         tot += Q;
         srv[q] = sv;

@@ -47,13 +47,49 @@ def k1_segment():
     q_off, w = inputs.snapshots_uniform(3, 600, 4, 10, 150000)
     ci = (np.arange(600) % 2).astype(np.uint16)
     h = es.es_load_profile(prof, cfgs)
+    os.environ["ES_K1"] = "seg"
     g = es.es_score_candidates(h, torch.from_numpy(q_off).to(DEV), torch.from_numpy(w).to(DEV),
                                torch.from_numpy(ci).to(DEV))
-    r = oracle.decide_batch(prof, cfgs, q_off, w, ci)
     torch.cuda.synchronize()
+    os.environ.pop("ES_K1")
+    r = oracle.decide_batch(prof, cfgs, q_off, w, ci)
     for k in ["m", "e", "B", "L", "S", "flags"]:
         assert np.array_equal(g[k].cpu().numpy(), r[k]), k
     return "k1 warp-segment: ok"
+
+
+def k1_thread():
+    """Thread-per-snapshot mapping: one SLO, regions over several shared-memory
+    chunks, a misaligned waits view, planted inversions (per-lane redo), a few
+    clip-path snapshots (handed to the warp segments), mixed SLOs in one warp."""
+    M = 8
+    prof = inputs.synth_profile(M, 5, list(range(1, 33)))
+    cfgs = [inputs.SchedCfg(tau=50000, b_max=32), inputs.SchedCfg(tau=90000, b_max=20)]
+    n = 32 * 9 + 5
+    q_off, w = inputs.snapshots_uniform(11, n, M, 60, 60000)
+    w = w.copy()
+    for s in (7, 100, 200):  # clip path
+        lo = int(q_off[s * M])
+        if int(q_off[s * M + 1]) > lo:
+            w[lo] = 200000
+    for s in (40, 150):  # inversions inside a queue
+        lo, hi = int(q_off[s * M + 2]), int(q_off[s * M + 3])
+        if hi - lo >= 3:
+            w[lo + 2] = w[lo + 1] + 1
+    ci = np.zeros(n, np.uint16)
+    ci[64 + 3] = 1
+    h = es.es_load_profile(prof, cfgs)
+    buf = np.zeros(w.size + 1, np.uint32)
+    buf[1:] = w
+    dw = torch.from_numpy(buf).to(DEV)[1:]
+    os.environ["ES_K1"] = "thread"
+    g = es.es_score_candidates(h, torch.from_numpy(q_off).to(DEV), dw, torch.from_numpy(ci).to(DEV))
+    torch.cuda.synchronize()
+    os.environ.pop("ES_K1")
+    r = oracle.decide_batch(prof, cfgs, q_off, w, ci)
+    for k in ["m", "e", "B", "L", "S", "flags"]:
+        assert np.array_equal(g[k].cpu().numpy(), r[k]), k
+    return "k1 thread per snapshot (balanced pass, chunks, misaligned, inversions, clip list, mixed SLOs): ok"
 
 
 def k1_stream(shallow):
@@ -82,6 +118,7 @@ CASES = {
     "cfg2_symphony": lambda: k2("cfg2", [1, 2, 3, 4], 1200, policy=7),
     "cfg2_grid": lambda: k2("cfg2", [1, 2], 600, policy=8),
     "k1_seg": k1_segment,
+    "k1_thread": k1_thread,
     "k1_stream": lambda: k1_stream(False),
     "k1_clip": lambda: k1_stream(True),
 }
