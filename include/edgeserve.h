@@ -137,7 +137,11 @@ typedef struct {
  * urgency tables on the GPU (reading Q5: x_c, r, A, Bt, H).  Synchronous.
  * Errors: ES_ERR_ARG, ES_ERR_PROFILE_GRID, ES_ERR_PROFILE_MONOTONE (the
  * message names (m, e, b)), ES_ERR_OUT_OF_GRID (b_max), ES_ERR_NUMERIC,
- * ES_ERR_CUDA, ES_ERR_OOM.  *out is NULL on failure.
+ * ES_ERR_CUDA, ES_ERR_OOM.  *out is NULL on failure.  Capacity: the kernels
+ * stage the image core (latency tables + per-cfg A / Bt, ~5.4 KB per cfg for
+ * tau = 100 ms) in shared memory and read the per-cfg H tables from global
+ * memory, so a handle holds as many cfgs as fit ~220 KB of core (about 38 for
+ * an 8 x 5 x 32 profile); beyond that ES_ERR_ARG asks to split the cfgs.
  */
 ES_API es_status es_load_profile(const es_profile_desc *desc, const es_sched_cfg *cfgs, int32_t ncfg,
                           int32_t device, es_profile **out);

@@ -208,10 +208,14 @@ es_status es_load_profile(const es_profile_desc *desc, const es_sched_cfg *cfgs,
     lay.c0_r4 = 4u * ((1024u - recs[0].tau % 1024u) % 1024u);
     lay.c0_amask = 4u * (p2 - 1u);
   }
+  // kernels stage the image core (everything but the per-cfg H tables, read from
+  // global memory) when the whole image would not fit or would cut residency
   const int smax = max_dyn_smem(device);
-  if ((int)lay.bytes + 64 > smax)
-    return fail(ES_ERR_ARG, "profile image of %u bytes exceeds %d bytes of shared memory per CTA (too many cfgs)",
-                lay.bytes, smax);
+  if ((int)lay.core_bytes + 4096 > smax)
+    return fail(ES_ERR_ARG,
+                "profile image core of %u bytes (tables of %d cfgs) exceeds %d bytes of shared memory per CTA: "
+                "split the cfgs over several handles",
+                lay.core_bytes, ncfg, smax);
 
   std::vector<uint8_t> img(lay.bytes, 0);
   memcpy(img.data() + lay.off_lat, desc->latency_us, 4u * cells);

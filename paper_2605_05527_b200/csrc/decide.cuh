@@ -586,24 +586,36 @@ __device__ __forceinline__ Decision decide_general(const Seg<LPS, MM> &sg, const
 //   srv_q = E_q - S_q (own served head tasks), Q_q = T_q - S_q (whole queue),
 // tot = sum over the segment's queues of Q_q.  Same integers as the fast path
 // of decide(); exact in any order.  Whole warp; `fast` must be warp-uniform.
-// Per-warp scratch (shared memory, FLAT_BYTES): the non-empty queues by rank.
-constexpr uint32_t FLAT_BYTES = 32 * 16 * 2 + 3 * 32 * 8;
+// Per-warp scratch (shared memory, FLAT_BYTES): one 16-byte descriptor per
+// non-empty queue by rank {queue address minus 4 x its flat start, t + r, A and
+// Bt word offsets}, and the running sums at each queue's start (slotS, by rank;
+// slotS[nq] = the warp's total, so a queue's total is slotS[r + 1] - slotS[r])
+// and after its served head (slotE).  A position's queue rank, and whether it
+// starts a queue or ends a served head, come from per-trip bit words that the
+// queue owners publish with one REDUX.OR each.
+constexpr uint32_t FLAT_BYTES = 32 * 16 + 33 * 8 + 32 * 8 + 8;
 #ifndef FLAT_WF
 #define FLAT_WF 2  // flat positions per lane per trip
 #endif
+
+__device__ __forceinline__ uint32_t lds_ro(uint32_t saddr) {  // staged tables: never written after staging
+  uint32_t v;
+  asm("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(saddr));
+  return v;
+}
 
 template <int LPS, int MM>
 __device__ __forceinline__ Decision decide_fast_flat(const Seg<LPS, MM> &sg, const SmemProf &P, const SmemCfg &C,
                                                     uint32_t len, const Cand &cand, const uint32_t *Ah, uint32_t t,
                                                     uint8_t *scratch) {
   constexpr int GL = Seg<LPS, MM>::GL;
-  uint4 *ent0 = reinterpret_cast<uint4 *>(scratch);  // {start, end, B | q << 16, t + r}
-  uint4 *ent1 = ent0 + 32;                            // {ptr lo, ptr hi, off_A, off_Bt}
-  uint64_t *slotS = reinterpret_cast<uint64_t *>(ent1 + 32);  // Pf at start_q, start_q + B_q, end_q
-  uint64_t *slotE = slotS + 32, *slotT = slotE + 32;
+  uint4 *ent = reinterpret_cast<uint4 *>(scratch);           // by rank
+  uint64_t *slotS = reinterpret_cast<uint64_t *>(ent + 32);  // [33]
+  uint64_t *slotE = slotS + 33;                               // [32]
   const uint32_t lane = (uint32_t)sg.lane;
+  const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(P.sm);
   const bool own = sg.gl == 0 && len > 0u;  // queue owner: lane 0 of a non-empty group
-  const uint32_t Bown = len ? cand.B : 0u;
+  const uint32_t Bown = len ? cand.B : 0u;  // 1 <= B* <= len (Eq. 5)
   // exclusive scan of the owners' lengths over the warp
   uint32_t incl = own ? len : 0u;
 #pragma unroll
@@ -612,13 +624,13 @@ __device__ __forceinline__ Decision decide_fast_flat(const Seg<LPS, MM> &sg, con
     if (lane >= (uint32_t)o) incl += v;
   }
   const uint32_t start = incl - (own ? len : 0u);
+  const uint32_t send = start + Bown - 1u;  // last position of the own served head
   const uint32_t NW = __shfl_sync(FULL, incl, 31);
   const unsigned ne = __ballot_sync(FULL, own);
+  const uint32_t orank = __popc(ne & ((1u << lane) - 1u));
   if (own) {
-    const uint32_t rk = __popc(ne & ((1u << lane) - 1u));
-    const uint64_t ptr = reinterpret_cast<uint64_t>(Ah);
-    ent0[rk] = make_uint4(start, start + len, Bown | (lane << 16), t + C.r);
-    ent1[rk] = make_uint4((uint32_t)ptr, (uint32_t)(ptr >> 32), C.off_A, C.off_Bt);
+    const uint64_t ptr = reinterpret_cast<uint64_t>(Ah) - 4ull * start;  // address of flat position f: ptr + 4 f
+    ent[orank] = make_uint4((uint32_t)ptr, (uint32_t)(ptr >> 32), t + C.r, (C.off_A >> 2) | ((C.off_Bt >> 2) << 16));
   }
   __syncwarp();
   uint64_t carry = 0ull;
@@ -629,21 +641,27 @@ __device__ __forceinline__ Decision decide_fast_flat(const Seg<LPS, MM> &sg, con
   constexpr int LPW = 32 / WF;  // lanes per 32-position word
   const uint32_t lw = lane / LPW, lb = (lane % LPW) * WF;  // this lane's word, its first bit in it
   for (uint32_t base = 0; base < NW; base += 32u * WF) {
-    // queue starts inside this trip: one bit per position, one word per 32
-    const uint32_t rel = start - base;
+    // queue starts and served-head ends inside this trip: one bit per position
+    const uint32_t rel = start - base, rel2 = send - base;
     const bool here = own && start >= base && rel < 32u * WF;
-    uint32_t pre = 0u, word = 0u, tripc = 0u;
+    const bool here2 = own && send >= base && rel2 < 32u * WF;
+    uint32_t pre = 0u, word = 0u, word2 = 0u, tripc = 0u;
 #pragma unroll
     for (int w = 0; w < WF; ++w) {
       const uint32_t bit = here && (rel >> 5) == (uint32_t)w ? 1u << (rel & 31u) : 0u;
-      uint32_t mw;
+      const uint32_t bit2 = here2 && (rel2 >> 5) == (uint32_t)w ? 1u << (rel2 & 31u) : 0u;
+      uint32_t mw, mw2;
       asm volatile("redux.sync.or.b32 %0, %1, 0xffffffff;" : "=r"(mw) : "r"(bit));
+      asm volatile("redux.sync.or.b32 %0, %1, 0xffffffff;" : "=r"(mw2) : "r"(bit2));
       const uint32_t c = __popc(mw);
       if ((uint32_t)w < lw) pre += c;
-      if ((uint32_t)w == lw) word = mw;
+      if ((uint32_t)w == lw) {
+        word = mw;
+        word2 = mw2;
+      }
       tripc += c;
     }
-    // G of the lane's positions; boundary roles packed with the queue id
+    // G of the lane's positions; boundary roles packed with the queue rank
     uint64_t gk[WF];
     uint32_t ik[WF];
     uint64_t lsum = 0ull;
@@ -656,18 +674,16 @@ __device__ __forceinline__ Decision decide_fast_flat(const Seg<LPS, MM> &sg, con
         const uint32_t bk = lb + (uint32_t)k;
         const uint32_t le = bk == 31u ? FULL : ((2u << bk) - 1u);
         const uint32_t rk = cb + pre + __popc(word & le) - 1u;
-        const uint4 e0 = ent0[rk], e1 = ent1[rk];
-        const uint32_t p = f - e0.x;
-        const uint32_t *qa = reinterpret_cast<const uint32_t *>((uint64_t)e1.x | ((uint64_t)e1.y << 32));
+        const uint4 e = ent[rk];
+        const uint32_t *qa = reinterpret_cast<const uint32_t *>((uint64_t)e.x | ((uint64_t)e.y << 32));
         // v = w + r = (t + r) - a; w < fast_lim <= x_c, so v >> 10 < nA (the
         // clamps of G_of are no-ops on the fast path)
-        const uint32_t v = e0.w - __ldg(qa + p);
-        const uint32_t A = *reinterpret_cast<const uint32_t *>(P.sm + e1.z + 4u * (v >> SBITS));
-        const uint32_t Bt = *reinterpret_cast<const uint32_t *>(P.sm + e1.w + 4u * (v & (S - 1u)));
+        const uint32_t v = e.z - __ldg(qa + f);
+        const uint32_t A = lds_ro(sbase + 4u * ((e.w & 0xFFFFu) + (v >> SBITS)));
+        const uint32_t Bt = lds_ro(sbase + 4u * ((e.w >> 16) + (v & (S - 1u))));
         gk[k] = ((uint64_t)A * (uint64_t)Bt) >> F;
         lsum += gk[k];
-        ik[k] = (e0.z >> 16) | (p == 0u ? 0x100u : 0u) | (p + 1u == (e0.z & 0xFFFFu) ? 0x200u : 0u) |
-                (f + 1u == e0.y ? 0x400u : 0u);
+        ik[k] = rk | (((word >> bk) & 1u) << 8) | (((word2 >> bk) & 1u) << 9);
       }
     }
     // running prefix over the flat order: exclusive scan of the lane sums
@@ -682,21 +698,21 @@ __device__ __forceinline__ Decision decide_fast_flat(const Seg<LPS, MM> &sg, con
     for (int k = 0; k < WF; ++k) {
       Pf += gk[k];  // prefix through this position
       if (ik[k] >> 8) {
-        const uint32_t q = ik[k] & 0xFFu;
-        if (ik[k] & 0x100u) slotS[q] = Pf - gk[k];
-        if (ik[k] & 0x200u) slotE[q] = Pf;
-        if (ik[k] & 0x400u) slotT[q] = Pf;
+        const uint32_t r = ik[k] & 0xFFu;
+        if (ik[k] & 0x100u) slotS[r] = Pf - gk[k];
+        if (ik[k] & 0x200u) slotE[r] = Pf;
       }
     }
     carry += __shfl_sync(FULL, s, 31);
     cb += tripc;
   }
+  if (lane == 0) slotS[__popc(ne)] = carry;
   __syncwarp();
   uint64_t srv = 0ull, Q = 0ull;
   if (own) {
-    const uint64_t s0 = slotS[lane];
-    srv = slotE[lane] - s0;
-    Q = slotT[lane] - s0;
+    const uint64_t s0 = slotS[orank];
+    srv = slotE[orank] - s0;
+    Q = slotS[orank + 1u] - s0;
   }
   const uint64_t tot = sg.sum64(Q);
   srv = sg.bcast(srv, sg.grp * GL);

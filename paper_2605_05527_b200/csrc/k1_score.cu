@@ -565,7 +565,6 @@ cudaError_t launch_score(const uint8_t *img, const ImgLayout &lay, const es_snap
   // many SLOs (image above 48 KB, e.g. cfg3's nine): stage only the core so
   // that 4 CTAs fit per SM; each candidate's H is one L1-cached global load
   a.stage_bytes = lay.bytes > 48u * 1024u ? lay.core_bytes : lay.bytes;
-  if (const char *env = getenv("ES_K1_STAGE")) a.stage_bytes = strcmp(env, "full") == 0 ? lay.bytes : lay.core_bytes;
   // deep snapshots (>= 1024 waits each on average): the three-phase stream;
   // Algorithm 1 on short snapshots: one thread per snapshot (clip-path ones
   // handed to the warp segments); the baseline policies and GRID: warp segments

@@ -74,8 +74,9 @@ __global__ void __launch_bounds__(256, 6) k1s_prep(const uint8_t *__restrict__ g
   pdl_trigger();
   extern __shared__ __align__(16) uint8_t smem[];
   __shared__ uint64_t mbar;
-  stage_image(smem, gimg, lay.bytes, &mbar);
-  const SmemProf P = smem_prof(smem, lay);
+  stage_image(smem, gimg, lay.core_bytes, &mbar);  // the core: H (one load per queue) stays in global memory
+  SmemProf P = smem_prof(smem, lay);
+  P.hb = gimg;
   const int M = P.M;
   const int64_t nq = a.n * M;
   const int lane = threadIdx.x & 31;
@@ -272,7 +273,7 @@ __global__ void __launch_bounds__(256, ES_K1_MINB) k1s_stream_fast(const uint8_t
   pdl_trigger();
   extern __shared__ __align__(16) uint8_t smem[];
   __shared__ uint64_t mbar;
-  stage_image(smem, gimg, lay.bytes, &mbar);
+  stage_image(smem, gimg, lay.core_bytes, &mbar);  // A and Bt: the core
   const SmemProf P = smem_prof(smem, lay);
   const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(smem);
   const int M = P.M;
@@ -455,7 +456,7 @@ __global__ void __launch_bounds__(TMA_NW * 32, 1) k1s_stream_tma(const uint8_t *
   }
   __syncwarp();
   for (int64_t k = 0; k < min((int64_t)rg.nsl - 1, npieces); ++k) issue(k, (uint32_t)k);
-  stage_image(smem, gimg, lay.bytes, &mbar);  // (also publishes the mbarrier inits)
+  stage_image(smem, gimg, lay.core_bytes, &mbar);  // A and Bt (also publishes the mbarrier inits)
   if (npieces == 0) return;
   const SmemProf P = smem_prof(smem, lay);
   // ---- initial queue: largest q < nq with q_off[q] <= first position of the range
@@ -926,14 +927,14 @@ template <int NW>
 cudaError_t launch_tma(const uint8_t *img, const ImgLayout &lay, const StreamArgs &a, int64_t nq, cudaStream_t st,
                        int sms, int optin, bool regs) {
   TmaRing rg{};
-  rg.ring_off = (lay.bytes + 127u) & ~127u;
+  rg.ring_off = (lay.core_bytes + 127u) & ~127u;
   const int64_t room = (int64_t)optin - 64 - rg.ring_off;
   for (uint32_t pv = PV_MAX; pv >= 128u && rg.nsl < 3u; pv >>= 1) {
     const int64_t per_slot = NW * (pv * 16 + 8);
     rg.pv = pv;
     rg.nsl = room > 0 ? (uint32_t)(room / per_slot < 6 ? room / per_slot : 6) : 0u;
   }
-  if (regs || rg.nsl < 2) return launch_persistent(k1s_stream_fast, img, lay, a, nq, 8, lay.bytes, st, sms);
+  if (regs || rg.nsl < 2) return launch_persistent(k1s_stream_fast, img, lay, a, nq, 8, lay.core_bytes, st, sms);
   rg.mbar_off = rg.ring_off + NW * rg.nsl * rg.pv * 16u;
   const size_t dyn = rg.mbar_off + NW * rg.nsl * 8u;
   // single SLO: table bases as parameters; the masked A index must stay inside dynamic smem
@@ -1002,7 +1003,7 @@ cudaError_t launch_score_stream(const uint8_t *img, const ImgLayout &lay, const 
   a.slow_list = reinterpret_cast<int64_t *>(sp + acc_bytes);
   a.rec = reinterpret_cast<QRec *>(sp + acc_bytes + list_bytes);
   e = cudaMemsetAsync(a.acc, 0, acc_bytes, st);
-  if (e == cudaSuccess) e = launch_persistent(k1s_prep, img, lay, a, nq, 256, lay.bytes, st, sms, false);
+  if (e == cudaSuccess) e = launch_persistent(k1s_prep, img, lay, a, nq, 256, lay.core_bytes, st, sms, false);
   if (e == cudaSuccess) e = launch_fast(img, lay, a, nq, st, sms);
   if (e == cudaSuccess) {
     if (lay.M <= 2) e = launch_persistent(k1s_clip<2>, img, lay, a, sn.n, 8, lay.core_bytes, st, sms);

@@ -591,6 +591,33 @@ def test_k1_policies(M):
     assert_k1_equal(run_k1(prof, cfgs, q_off, w, ci), oracle.decide_batch(prof, cfgs, q_off, w, ci), M)
 
 
+@pytest.mark.parametrize("mode", ["thread", "seg", "stream"])
+def test_many_slos_core_staging(monkeypatch, mode):
+    """24 SLO cfgs (tau 20..135 ms) on the 8 x 5 x 32 profile: the whole image
+    (~390 KB) exceeds shared memory, so every kernel stages the core and reads
+    H from global memory -- K1 on every mapping and K2, against the oracle."""
+    monkeypatch.setenv("ES_K1", mode)
+    prof = inputs.synth_profile(8, 5, list(range(1, 33)))
+    cfgs = [inputs.SchedCfg(tau=20000 + 5000 * k, b_max=32) for k in range(24)]
+    M, n = 8, 200
+    depth = 1500 if mode == "stream" else 40
+    q_off, wts = inputs.snapshots_poisson_depth(31, np.arange(n), M, depth, [depth / 90000.0] * M)
+    ci = (np.arange(n) % 24).astype(np.uint16)
+    h = es.es_load_profile(prof, cfgs)
+    o = es.es_score_candidates(h, to_dev(q_off, torch.uint64), to_dev(wts, torch.uint32), to_dev(ci, torch.uint16))
+    torch.cuda.synchronize()
+    assert_k1_equal({k: np_of(v) for k, v in o.items()}, oracle.decide_batch(prof, cfgs, q_off, wts, ci), M)
+    if mode == "thread":  # K2 replay under the same 24 cfgs (cfg3-shaped traces, cfg index s mod 24)
+        w = inputs.workload("cfg3", scen_ids=list(range(0, 96, 4)), n_req=1200)
+        tr = w.traces
+        tr.cfg_idx = (np.arange(tr.n_scen) % 24).astype(np.uint16)
+        w2 = inputs.Workload("slo24", prof, cfgs, tr, 0)
+        g = run_k2(w2, dec_cap=1500)
+        ref = oracle.replay_batch(prof, cfgs, tr, dec_cap=1500, nthreads=8)
+        assert g["_code"] == 0
+        assert_k2_equal(g, ref, 1500)
+
+
 @pytest.mark.parametrize("fast", ["tma", "regs"])
 def test_k1_stream_large_image(monkeypatch, fast):
     """Deep snapshots under cfg3's nine SLOs (20..100 ms): the profile image
