@@ -767,6 +767,8 @@ __global__ void __launch_bounds__(256) k1s_clip(const uint8_t *__restrict__ gimg
     const uint32_t minthr = redux_min(rthr);
     uint64_t T = 0ull;  // G over the rows below every threshold
     bool bad = false;
+    const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(smem);
+    const GTab G{sbase + C.off_A, sbase + C.off_Bt, 4u * C.r, C.nA1};  // w < x_c in the read window (else flagged)
     for (int q = 0; q < M; ++q) {  // warp-uniform
       const uint32_t len = __shfl_sync(FULL, rlen, q), c = __shfl_sync(FULL, rc, q);
       if (len <= c) continue;
@@ -774,16 +776,18 @@ __global__ void __launch_bounds__(256) k1s_clip(const uint8_t *__restrict__ gimg
       const uint32_t *W = a.waits + __shfl_sync(FULL, rlo, q);
       uint32_t carry = 0xFFFFFFFFu;  // no predecessor check at the first live wait
       for (uint32_t p0 = c; p0 < len; p0 += 32u * CLIP_ROWS) {  // warp-uniform
+        const uint32_t *Wp = W + p0 + lane;
+        const uint32_t nr = min((len - p0 + 31u) / 32u, (uint32_t)CLIP_ROWS);  // rows in this window
         uint32_t wv[CLIP_ROWS];
 #pragma unroll
         for (int j = 0; j < CLIP_ROWS; ++j) {
-          const uint32_t p = p0 + 32u * j + lane;
-          wv[j] = p < len ? __ldg(W + p) : 0u;
+          wv[j] = 0u;
+          if ((uint32_t)j < nr && p0 + 32u * j + lane < len) wv[j] = __ldg(Wp + 32 * j);
         }
 #pragma unroll
         for (int j = 0; j < CLIP_ROWS; ++j) {
+          if ((uint32_t)j >= nr) break;
           const uint32_t r0 = p0 + 32u * j;
-          if (r0 >= len) break;
           const uint32_t p = r0 + lane, w = wv[j];
           uint32_t prev = __shfl_up_sync(FULL, w, 1);
           if (lane == 0) prev = carry;
@@ -791,12 +795,12 @@ __global__ void __launch_bounds__(256) k1s_clip(const uint8_t *__restrict__ gimg
           const uint32_t rowmax = __shfl_sync(FULL, w, 0);
           const bool valid = p < len;
           bad |= valid && (w > prev || w >= C.x_c);
+          const uint32_t gw = valid ? G(w) : 0u;
           if (rowmax < minthr && r0 >= B) {  // below every threshold, no served task
-            if (valid) T += G_of(P, C, w);
+            T += gw;
             continue;
           }
           if (!valid) continue;
-          const uint32_t gw = G_of(P, C, w);
 #pragma unroll
           for (int m = 0; m < MM; ++m) {
             if (m == q && p < B) continue;  // candidate q's own served tasks

@@ -15,7 +15,12 @@ kname = rows[0][1]
 h = rows[1]
 ia, isrc, iex, iss = h.index("Address"), h.index("Source"), h.index("Instructions Executed"), \
     h.index("Warp Stall Sampling (All Samples)")
-data = [(int(r[ia], 16), r[isrc], float(r[iex] or 0), float(r[iss] or 0)) for r in rows[2:] if len(r) >= len(h)]
+body = []
+for r in rows[2:]:  # the first kernel's block only (a report may hold several)
+    if r and r[0] in ("Kernel Name", "Address"):
+        break
+    body.append(r)
+data = [(int(r[ia], 16), r[isrc], float(r[iex] or 0), float(r[iss] or 0)) for r in body if len(r) >= len(h)]
 base = data[0][0]
 # find the cubin function
 tmp = tempfile.mkdtemp()

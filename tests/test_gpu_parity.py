@@ -516,6 +516,65 @@ def test_k1_full_size_bench_batch():
     assert np.array_equal(cand[ok].min(axis=1), g["S"][ok])
 
 
+def _tiled_sample_parity(prof, cfgs, q_off, w0, ci, tiles, n_sample, seed):
+    """bench.k1_line's launch on the distinct snapshots (q_off, w0, ci) repeated
+    `tiles` times back to back, then n_sample snapshots spread over every tile
+    against the oracle element by element (their queues re-packed into a small
+    CSR), plus the argmin property on every snapshot."""
+    M = prof.M
+    n0 = (q_off.size - 1) // M
+    nw = np.uint64(w0.size)
+    q = np.concatenate([q_off[:-1] + np.uint64(t) * nw for t in range(tiles)] + [q_off[-1:] + np.uint64(tiles - 1) * nw])
+    h = es.es_load_profile(prof, cfgs)
+    dci = None if ci is None else to_dev(np.tile(ci, tiles), torch.uint16)
+    o = es.es_score_candidates(h, to_dev(q, torch.uint64), to_dev(w0, torch.uint32).repeat(tiles), dci)
+    torch.cuda.synchronize()
+    g = {k: np_of(v) for k, v in o.items()}
+    rng = np.random.default_rng(seed)
+    ids = np.sort(rng.choice(n0 * tiles, n_sample, replace=False))
+    sub_off, parts = [0], []
+    for s in ids:
+        s0 = s % n0
+        for m in range(M):
+            lo, hi = int(q_off[s0 * M + m]), int(q_off[s0 * M + m + 1])
+            parts.append(w0[lo:hi])
+            sub_off.append(sub_off[-1] + hi - lo)
+    sub_ci = None if ci is None else ci[ids % n0]
+    ref = oracle.decide_batch(prof, cfgs, np.array(sub_off, np.uint64), np.concatenate(parts), sub_ci)
+    sub = {k: g[k][ids] for k in ["m", "e", "B", "L", "S", "flags"]}
+    sub["cand"] = g["cand"].reshape(-1, M)[ids]
+    assert_k1_equal(sub, ref, M)
+    cand = g["cand"].reshape(-1, M)
+    ok = g["flags"] & 6 == 0
+    assert np.array_equal(np.argmin(cand[ok], axis=1), g["m"][ok].astype(np.int64))
+    assert np.array_equal(cand[ok].min(axis=1), g["S"][ok])
+    return g
+
+
+def test_k1_clip_bench_batch():
+    """K1 at the bench's `k1_clip` size and launch (bench.bench_k1_clip: 5-C
+    depth at 5-B overload rates, 262,144 snapshots, every one on the clip path:
+    k1s_prep + k1s_clip + k1s_finish): 256 sampled snapshots against the oracle."""
+    prof = inputs.synth_profile(8, 5, list(range(1, 33)))
+    cfgs = [inputs.SchedCfg(tau=50000, b_max=32)]
+    rate = inputs.rates_for_shallow_load(prof, 32, 1.5)
+    q_off, w0 = inputs.snapshots_poisson_depth(2000, np.arange(4096), 8, 4096, rate)
+    g = _tiled_sample_parity(prof, cfgs, q_off, w0, None, 64, 256, 5)
+    assert (g["flags"] & 1).sum() == 0  # overload: nothing feasible, as in the bench line
+
+
+def test_k1_harvested_bench_batch():
+    """K1 at the bench's `k1_harvested` size and launch (bench.k1_harvested_batch:
+    every decision instant of 512 cfg3 replays, nine SLOs, 8 tiles, the
+    thread-per-snapshot mapping): 512 sampled snapshots against the oracle."""
+    import bench
+    from paper_2605_05527_b200 import engine
+    dev = torch.device(DEV)
+    _, q_off, w0, ci, _ = bench.k1_harvested_batch(es, engine, dev, torch.cuda.current_stream(dev), 0, 512)
+    w = inputs.workload("cfg3", scen_ids=[0], n_req=10)
+    _tiled_sample_parity(w.profile, w.cfgs, q_off, w0, ci, 8, 512, 6)
+
+
 # ------------------------------------------------------------------ baseline / ablation policies (Q26)
 
 POLICY_IDS = {"edgeserving": 0, "all_final": 1, "all_early": 2, "ee_lqf": 3, "ee_edf": 4, "allfinal_da": 5,
