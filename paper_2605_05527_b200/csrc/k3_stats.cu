@@ -182,31 +182,32 @@ __global__ void __launch_bounds__(NT) k3_stats(StatsArgs a) {
     // take no per-element test, the (at most two) edge quads do
     const uint4 *v4 = reinterpret_cast<const uint4 *>(vals);
     const uint32_t nq = (n + off + 3u) / 4u;
+    // latencies crowd a few 4.096 ms bins: the updates are warp-aggregated
+    // (one shared atomic per distinct bin per warp, __match_any) instead of
+    // serialising on the same address
+    auto add_bin = [&](uint32_t bin) {  // whole warp; bin = 0xFFFFFFFF: no value
+      const unsigned peers = __match_any_sync(0xffffffffu, bin);
+      if (bin != 0xFFFFFFFFu && (threadIdx.x & 31) == (uint32_t)(__ffs(peers) - 1)) atomicAdd(&hist[bin], (uint32_t)__popc(peers));
+    };
     if (staged) {
-      for (uint32_t q = threadIdx.x; q < nq; q += NT) {
-        const uint4 x = v4[q];
+      for (uint32_t q0 = threadIdx.x & ~31u; q0 < nq; q0 += NT) {  // warp-uniform trip count
+        const uint32_t q = q0 + (threadIdx.x & 31);
+        const uint4 x = q < nq ? v4[q] : make_uint4(0u, 0u, 0u, 0u);
         const uint32_t j = 4u * q;
-        if (j >= off && j + 4u <= n + off) {
-          mx = max(max(mx, max(x.x, x.y)), max(x.z, x.w));
-          atomicAdd(&hist[min(x.x >> 12, COARSE_OVF)], 1u);
-          atomicAdd(&hist[min(x.y >> 12, COARSE_OVF)], 1u);
-          atomicAdd(&hist[min(x.z >> 12, COARSE_OVF)], 1u);
-          atomicAdd(&hist[min(x.w >> 12, COARSE_OVF)], 1u);
-        } else {
-          const uint32_t e[4] = {x.x, x.y, x.z, x.w};
+        const uint32_t e[4] = {x.x, x.y, x.z, x.w};
 #pragma unroll
-          for (int c = 0; c < 4; ++c)
-            if (j + c >= off && j + c < n + off) {
-              mx = max(mx, e[c]);
-              atomicAdd(&hist[min(e[c] >> 12, COARSE_OVF)], 1u);
-            }
+        for (int c = 0; c < 4; ++c) {
+          const bool in = q < nq && j + c >= off && j + c < n + off;
+          if (in) mx = max(mx, e[c]);
+          add_bin(in ? min(e[c] >> 12, COARSE_OVF) : 0xFFFFFFFFu);
         }
       }
     } else {
-      for (uint32_t i = threadIdx.x; i < n; i += NT) {
-        const uint32_t v = __ldg(gsrc + i);
-        mx = max(mx, v);
-        atomicAdd(&hist[min(v >> 12, COARSE_OVF)], 1u);
+      for (uint32_t i0 = threadIdx.x & ~31u; i0 < n; i0 += NT) {
+        const uint32_t i = i0 + (threadIdx.x & 31);
+        const uint32_t v = i < n ? __ldg(gsrc + i) : 0u;
+        if (i < n) mx = max(mx, v);
+        add_bin(i < n ? min(v >> 12, COARSE_OVF) : 0xFFFFFFFFu);
       }
     }
     mx = __reduce_max_sync(0xffffffffu, mx);
