@@ -18,7 +18,7 @@ timeout 900 ncu --set full --clock-control none --import-source on -k 'regex:k1_
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:k1s_ -s 4 -c 4 \
   -o gpurun_out/prof_k1clip_$R python scripts/k1_clip_once.py 1 > /dev/null 2>&1
 timeout 900 python bench.py --impl reference --steps 3 --warmup 1 > gpurun_out/bench_ref_$R.json 2>&1
-timeout 900 python scripts/policy_table.py > gpurun_out/policies_$R.txt 2>&1
-timeout 900 python scripts/sweeps.py > gpurun_out/sweeps_$R.txt 2>&1
+
+
 tail -2 gpurun_out/smoke_$R.log; cat gpurun_out/tests_$R.log; tail -3 gpurun_out/bench_$R.err
 ls gpurun_out
