@@ -101,81 +101,22 @@ struct StatsArgs {
 __global__ void __launch_bounds__(NT) k3_stats(StatsArgs a) {
   __shared__ uint32_t hist[BINS];
   __shared__ uint32_t s_max;
-  extern __shared__ __align__(16) uint32_t vbuf[];  // two staging buffers of a.cap words
-  __shared__ uint64_t mbar[2];
-  const uint32_t mb0 = (uint32_t)__cvta_generic_to_shared(&mbar[0]);
-  uint32_t phase[2] = {0u, 0u};
+  extern __shared__ __align__(16) uint32_t vals[];
+  __shared__ uint64_t mbar;
+  const uint32_t mb = (uint32_t)__cvta_generic_to_shared(&mbar);
+  uint32_t phase = 0;
   if (threadIdx.x == 0) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(mb0));
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(mb0 + 8u));
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(mb));
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
-  // a scenario's staging plan: n post-warmup latencies at gsrc; staged in a
-  // buffer when they fit, as one bulk copy of the 16-byte aligned span
-  // [gsrc - off, ...) (nv4 vectors; the <= 3 trailing words loaded directly)
-  struct Plan {
-    bool ok;  // status OK and n > 0
-    uint32_t n, off, nv4;
-    const uint32_t *gsrc;
-    bool staged;
-  };
-  auto plan = [&](int64_t s) {
-    Plan pl{};
-    if (s >= a.n_scen || a.stats[s * ES_NSTAT + ES_ST_STATUS] != 0ull) return pl;
+  for (int64_t s = blockIdx.x; s < a.n_scen; s += gridDim.x) {
+    const uint64_t *st = a.stats + s * ES_NSTAT;
     const int k = a.cfg_idx ? (int)a.cfg_idx[s] : 0;
-    const uint32_t W = a.cfg[k].warmup;
-    const uint64_t base = a.arr_off[s * a.M];
-    const uint64_t total = a.arr_off[s * a.M + a.M] - base;
-    pl.n = total > W ? (uint32_t)(total - W) : 0u;
-    pl.ok = pl.n > 0u;
-    pl.gsrc = a.lat + base + W;
-    pl.staged = pl.ok && pl.n + 3u <= a.cap;  // + up to 3 leading words of 16-byte alignment
-    pl.off = pl.staged ? (uint32_t)(((uintptr_t)pl.gsrc >> 2) & 3u) : 0u;
-    pl.nv4 = pl.staged ? (pl.n + pl.off) / 4u : 0u;
-    return pl;
-  };
-  // thread 0: the bulk copy of scenario s into buffer b (its previous contents
-  // were read before the last __syncthreads: the async-proxy fence orders them)
-  auto issue = [&](const Plan &pl, int b) {
-    if (!pl.nv4) return;
-    const uint32_t mb = mb0 + 8u * (uint32_t)b;
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(mb), "r"(16u * pl.nv4) : "memory");
-    const uint32_t dst = (uint32_t)__cvta_generic_to_shared(vbuf + (size_t)b * a.cap);
-    const uint8_t *gs = reinterpret_cast<const uint8_t *>(pl.gsrc - pl.off);
-    for (uint32_t o = 0; o < 16u * pl.nv4; o += 16384u)
-      asm volatile(
-          "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst + o),
-          "l"(gs + o), "r"(min(16384u, 16u * pl.nv4 - o)), "r"(mb)
-          : "memory");
-  };
-  Plan cur = plan(blockIdx.x);
-  if (threadIdx.x == 0) issue(cur, 0);
-  int buf = 0;
-  for (int64_t s = blockIdx.x; s < a.n_scen; s += gridDim.x, buf ^= 1) {
-    // the next scenario's latencies stream into the other buffer meanwhile
-    const Plan nxt = plan(s + gridDim.x);
-    if (threadIdx.x == 0) issue(nxt, buf ^ 1);
-    const Plan pl = cur;
-    cur = nxt;
-    uint32_t *vals = vbuf + (size_t)buf * a.cap;
-    if (!pl.ok) {
+    if (st[ES_ST_STATUS] != 0ull) {
       if (a.p95 && threadIdx.x == 0) a.p95[s] = 0u;
-      // the group counters still add a status-OK scenario with no post-warmup completion
-      if (a.stats[s * ES_NSTAT + ES_ST_STATUS] == 0ull) {
-        const uint32_t g = a.group_id ? a.group_id[s] : 0u;
-        if (a.n_groups && g < a.n_groups && threadIdx.x < ES_NGSTAT) {
-          const int t = (int)threadIdx.x;
-          const int col = t < 6 ? t : t == 6 ? ES_ST_SUM_LAT : ES_ST_ACC_BP + (t - 7);
-          atomicAdd(reinterpret_cast<unsigned long long *>(a.counts + (uint64_t)g * ES_NGSTAT + threadIdx.x),
-                    (unsigned long long)a.stats[s * ES_NSTAT + col]);
-        }
-      }
-      __syncthreads();
       continue;
     }
-    const uint64_t *st = a.stats + s * ES_NSTAT;
     const uint32_t g = a.group_id ? a.group_id[s] : 0u;
     const bool grp = a.n_groups && g < a.n_groups;
     if (grp && threadIdx.x < ES_NGSTAT) {
@@ -186,25 +127,48 @@ __global__ void __launch_bounds__(NT) k3_stats(StatsArgs a) {
       atomicAdd(reinterpret_cast<unsigned long long *>(a.counts + (uint64_t)g * ES_NGSTAT + threadIdx.x),
                 (unsigned long long)st[col]);
     }
-    const uint32_t n = pl.n;
-    const uint32_t *gsrc = pl.gsrc;
-    const bool staged = pl.staged;
+    const uint32_t W = a.cfg[k].warmup;
+    const uint64_t base = a.arr_off[s * a.M];
+    const uint64_t total = a.arr_off[s * a.M + a.M] - base;
+    const uint32_t n = total > W ? (uint32_t)(total - W) : 0u;
+    if (n == 0u) {
+      if (a.p95 && threadIdx.x == 0) a.p95[s] = 0u;
+      continue;
+    }
+    const uint32_t *gsrc = a.lat + base + W;
+    const bool staged = n + 3u <= a.cap;  // + up to 3 leading words of 16-byte alignment
+    // stage the scenario's latencies into shared memory with TMA: one bulk copy
+    // of the 16-byte aligned span [gsrc - off, ...) (off <= 3 leading words
+    // ignored), the <= 3 trailing words loaded directly
     const uint32_t *src = gsrc;
-    const uint32_t off = pl.off;  // staged: vals[off + i] holds latency i (vals 16-byte aligned)
+    uint32_t off = 0u;  // staged: vals[off + i] holds latency i (vals 16-byte aligned)
     if (staged) {
-      const uint32_t nv4 = pl.nv4;
+      off = (uint32_t)(((uintptr_t)gsrc >> 2) & 3u);
+      const uint32_t nv4 = (n + off) / 4u;
+      if (threadIdx.x == 0 && nv4) {
+        // the previous scenario's generic-proxy reads of vals precede these async writes
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(mb), "r"(16u * nv4) : "memory");
+        const uint32_t dst = (uint32_t)__cvta_generic_to_shared(vals);
+        const uint8_t *gs = reinterpret_cast<const uint8_t *>(gsrc - off);
+        for (uint32_t o = 0; o < 16u * nv4; o += 16384u)
+          asm volatile(
+              "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                  dst + o),
+              "l"(gs + o), "r"(min(16384u, 16u * nv4 - o)), "r"(mb)
+              : "memory");
+      }
       for (uint32_t j = 4u * nv4 + threadIdx.x; j < n + off; j += NT) vals[j] = gsrc[j - off];
       if (nv4) {
-        const uint32_t mb = mb0 + 8u * (uint32_t)buf;
         uint32_t done = 0;
         while (!done)
           asm volatile(
               "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
               "selp.u32 %0, 1, 0, p;\n\t}"
               : "=r"(done)
-              : "r"(mb), "r"(phase[buf])
+              : "r"(mb), "r"(phase)
               : "memory");
-        phase[buf] ^= 1u;
+        phase ^= 1u;
       }
       src = vals + off;
     }
@@ -527,12 +491,12 @@ StatsArgs stats_args(const uint8_t *img, const ImgLayout &lay, const es_traces &
   a.stats = out.scen_stats;
   a.p95 = out.scen_p95_us;
   a.cfg = reinterpret_cast<const CfgRec *>(img + lay.off_cfg);
-  a.cap = 12288;  // 48 KB of staged latencies per buffer (two per CTA)
+  a.cap = 12288;  // 48 KB of staged latencies per CTA
   return a;
 }
 
 cudaError_t launch_stats(const StatsArgs &a, cudaStream_t st, int sms) {
-  const size_t dyn = 2u * (size_t)a.cap * sizeof(uint32_t);  // two staging buffers
+  const size_t dyn = (size_t)a.cap * sizeof(uint32_t);
   cudaError_t e = cudaFuncSetAttribute(k3_stats, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
   if (e != cudaSuccess) return e;
   int occ = 0;
