@@ -486,7 +486,9 @@ def main():
     achieved = ops / k2_avg_s
     alg_bytes = 4 * total + 4 * total + 8 * es.ES_NSTAT * S + 8 * (S * w.profile.M + 1)
     roof = {"bound": "alu", "achieved": achieved / 1e9, "peak": peak_ops / 1e9, "unit": "Gop/s",
-            "frac": achieved / peak_ops, "traffic": ncu_traffic("k2_replay_" + args.workload),
+            "frac": achieved / peak_ops,
+            "traffic": ncu_traffic("k2_replay_" + args.workload) or (ncu_traffic("k2_replay") if args.workload == "cfg3"
+                                                                      else None),
             "kernel": "k2_replay", "k2_ms": kms["k2"], "k2_share_of_step": kms["k2"] / (ms / args.steps),
             "peak_source": f"148 SM x 4 SMSP x 32 lanes x {sm_max:.0f} MHz ({src} sm_max): SURVEY 8(d)'s issue "
                            "peak in thread-instruction units",
@@ -495,6 +497,12 @@ def main():
                              "candidate + 4 per request + 2 per decision, counted exactly by the kernel",
             "hbm_view": {"alg_bytes_per_launch": alg_bytes, "achieved_gbs": alg_bytes / k2_avg_s / 1e9,
                          "peak_gbs": hbm, "frac": alg_bytes / k2_avg_s / 1e9 / hbm}}
+    iss = ncu_issue("k2_replay") if args.workload == "cfg3" else None
+    if iss and iss.get("warp_inst"):  # issue-slot evidence of the committed capture of this workload
+        roof["issue_view"] = {"issue_active_pct": iss["issue_active_pct"], "warp_inst_per_launch": iss["warp_inst"],
+                              "warp_inst_per_decision": iss["warp_inst"] / float(ssum["decisions"]),
+                              "source": "profiles/ncu_traffic.json (_issue; ncu --set full of bench.py, "
+                                        "profiles/r02_ncu_k2.txt)"}
     k3_bytes = 4 * total + 8 * es.ES_NSTAT * S  # K3 reads every latency once (+ the per-scenario counters)
     kernels = {"k2_ms": kms["k2"], "k3_ms": kms["k3"], "merge_ms": kms["merge"],
                "k3_gbs": k3_bytes / (kms["k3"] / 1e3) / 1e9,
