@@ -478,7 +478,7 @@ cudaError_t launch_t(const uint8_t *img, const ImgLayout &lay, const ReplayArgs 
     if (e != cudaSuccess) return e;
     // (and only while the extra per-CTA image copies leave L1 room: the
     // pending waits are re-read from L1 every decision)
-    if (o * t >= occ * 256 && (size_t)o * dyn_of(t) <= 72u * 1024u) {
+    if (o * t >= occ * 256 && (size_t)o * dyn_of(t) <= 96u * 1024u) {
       threads = t;
       occ = o;
       break;
