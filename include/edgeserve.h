@@ -168,8 +168,10 @@ typedef struct {
                                q_off[s*M+m+1])                                      */
   const uint32_t *waits_us; /* head (oldest) first, non-increasing per queue (Q7)  */
   int64_t n_waits;          /* q_off[n*M] if known (host value), else 0.  Selects the
-                               mapping: >= 1024 waits per snapshot on average -> one
-                               CTA per snapshot (deep queues), else a warp segment     */
+                               mapping: >= 1024 waits per snapshot on average -> the
+                               streamed three-phase mapping (deep queues), else one
+                               thread per snapshot (Algorithm 1; warp segments for the
+                               baseline policies and GRID).  Results never depend on it */
 } es_snapshots;
 
 #define ES_FLAG_FEASIBLE 1u  /* Eq. 6 satisfiable for the chosen model            */
