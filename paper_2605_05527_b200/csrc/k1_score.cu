@@ -283,6 +283,10 @@ __global__ void __launch_bounds__(K1T_THREADS, 1) k1_thread(const uint8_t *__res
 #pragma unroll
       for (int q = 0; q <= MM; ++q) rel[q] = live ? (uint32_t)(off[q] - R0) : 0u;
     }
+    uint32_t relM = 0u;  // rel[M]: this snapshot's end in the region
+#pragma unroll
+    for (int q = 0; q <= MM; ++q)
+      if (q == M) relM = rel[q];
     {  // L2 prefetch of the next group's waits region (its bounds loaded at the top)
       const uint64_t n0 = __shfl_sync(FULL, nb, 0), n1 = __shfl_sync(FULL, nb, 31);
       const char *nw = reinterpret_cast<const char *>(a.waits + n0);
@@ -351,7 +355,7 @@ __global__ void __launch_bounds__(K1T_THREADS, 1) k1_thread(const uint8_t *__res
         const uint32_t ce = min(cb + cap, nrel);
         for (uint32_t j = lane; j < cap / 32u; j += 32u) asm volatile("st.shared.u32 [%0], 0;" ::"r"(sBits + 4u * j));
         __syncwarp();
-        if (live) {  // queue starts of this chunk (no predecessor check there, Q24)
+        if (live && relM + mis >= cb && rel[0] + mis < ce) {  // queue starts of this chunk (no predecessor check, Q24)
 #pragma unroll
           for (int q = 0; q < MM; ++q) {
             const uint32_t x = rel[q] + mis;
@@ -411,7 +415,7 @@ __global__ void __launch_bounds__(K1T_THREADS, 1) k1_thread(const uint8_t *__res
           carry += __shfl_sync(FULL, sc, 31);
         }
         __syncwarp();
-        if (active) {  // this lane's queue boundaries inside the chunk
+        if (active && relM + mis >= cb && rel[0] + mis < ce) {  // this lane's queue boundaries inside the chunk
 #pragma unroll
           for (int q = 0; q <= MM; ++q) {
             if (q > M) continue;
@@ -430,7 +434,7 @@ __global__ void __launch_bounds__(K1T_THREADS, 1) k1_thread(const uint8_t *__res
         }
         __syncwarp();
       }
-      if (active) {  // boundaries at the region's end: E = the final running sum
+      if (active && relM + mis == nrel) {  // boundaries at the region's end (the last lane): E = the final sum
 #pragma unroll
         for (int q = 0; q <= MM; ++q) {
           if (q > M) continue;
