@@ -1,13 +1,19 @@
-// k1_score.cu -- K1: independent scheduling decisions on queue snapshots.
+// k1_score.cu -- K1: independent scheduling decisions on queue snapshots
+// (Algorithm 1, on the system state of S:112-115).  Two mappings:
 //
-// One warp segment of LPS lanes per snapshot (grid-stride), model g's queue
-// owned by lane group g (decide.cuh).  Per snapshot the segment reads the
-// (M+1) CSR offsets, the head wait of every queue and the live window of every
-// queue -- tasks whose wait is already >= x_c are clipped for every candidate
-// (Eq. 3) and are counted from the index by a GL-ary search on the
-// non-increasing waits (reading Q7), never read.  This is the HBM-streaming
-// form of the stability-score evaluation: no loop-carried state between
-// snapshots.
+// k1_thread (Algorithm 1, short snapshots; the default below 1,024 waits per
+//   snapshot): one thread per snapshot for the per-queue logic, one balanced
+//   pass of the warp for the Eq. 3-4 sums (see the comment above it).
+// k1_score (warp segments): one segment of LPS lanes per snapshot
+//   (grid-stride), model g's queue owned by lane group g (decide.cuh); used
+//   for the baseline policies and GRID, and for k1_thread's clip-path list.
+//   Per snapshot the segment reads the (M+1) CSR offsets, the head wait of
+//   every queue and the live window of every queue -- tasks whose wait is
+//   already >= x_c are clipped for every candidate (Eq. 3) and are
+//   counted from the index by a GL-ary search on the non-increasing waits
+//   (reading Q7), never read.
+// Deep snapshots (>= 1,024 waits on average) take the streamed mapping of
+// k1_stream.cu.  All mappings compute the same integers (tested invariant).
 #include <cuda_runtime.h>
 
 #include <algorithm>
