@@ -465,6 +465,22 @@ def test_k2_segment_widths(monkeypatch, lps):
     test_k2_errors()
 
 
+@pytest.mark.parametrize("M", [1, 3, 5])
+def test_k1_thread_balanced_pass_small_m(monkeypatch, M):
+    """The balanced pass with fewer models than the template width (M < 8, 4,
+    2: queues past M absent), one SLO and no cfg index array, regions over
+    several chunks, empty queues and a ragged batch, against the oracle."""
+    monkeypatch.setenv("ES_K1", "thread")
+    prof = inputs.synth_profile(M, 4, list(range(1, 17)))
+    cfgs = [inputs.SchedCfg(tau=60000, b_max=16)]
+    n = 32 * 11 + 13
+    q_off, w = inputs.snapshots_uniform(90 + M, n, M, 90, 80000)
+    h = es.es_load_profile(prof, cfgs)
+    o = es.es_score_candidates(h, to_dev(q_off, torch.uint64), to_dev(w, torch.uint32))
+    torch.cuda.synchronize()
+    assert_k1_equal({k: np_of(v) for k, v in o.items()}, oracle.decide_batch(prof, cfgs, q_off, w), M)
+
+
 @pytest.mark.parametrize("mode", ["stream", "thread", "seg"])
 def test_k1_all_mappings(monkeypatch, mode):
     """K1's mappings (3-phase streaming and one CTA per snapshot for deep
