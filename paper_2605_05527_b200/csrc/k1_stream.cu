@@ -38,7 +38,8 @@ constexpr uint64_t F_SLOW = 1, F_BAD = 2;
 #ifndef ES_K1_MINB
 #define ES_K1_MINB 4
 #endif
-constexpr uint32_t V4_LIM = (1u << 30) - 1024u;  // fast-stream G needs 4 (x_c + 1023) < 2^32
+constexpr uint32_t V4_LIM = (1u << 30) - 1024u;
+  // fast-stream G needs 4 (x_c + 1023) < 2^32
 
 struct StreamArgs {
   int64_t n;
@@ -102,13 +103,33 @@ __global__ void __launch_bounds__(256, 6) k1s_prep(const uint8_t *__restrict__ g
       const uint32_t *W = a.waits + r.lo;
       const uint32_t wmax = __ldg(W);
       if (wmax >= C.x_c) {  // clipped-for-everyone prefix: first position with w < x_c
-        uint32_t plo = 0, phi = r.len;
-        while (phi - plo > 1u) {
-          const uint32_t mid = plo + (phi - plo) / 2u;
-          if (__ldg(W + mid) >= C.x_c) plo = mid;
-          else phi = mid;
+        // interpolation on the waits (near-linear in position: Poisson
+        // arrivals), alternated with bisection so the worst case stays
+        // logarithmic; the bracket W[plo] >= x_c > W[phi] holds throughout, so
+        // the result is the exact boundary (counted, never summed: Q24)
+        const uint32_t wl = __ldg(W + r.len - 1u);
+        if (wl >= C.x_c) {
+          r.c = r.len;
+        } else {
+          uint32_t plo = 0, phi = r.len - 1u, wlo = wmax, whi = wl;
+          bool interp = true;
+          while (phi - plo > 1u) {
+            uint32_t mid = plo + (phi - plo) / 2u;
+            if (interp)  // wlo >= x_c > whi, so wlo > whi
+              mid = plo + 1u + (uint32_t)((float)(wlo - C.x_c) / (float)(wlo - whi) * (float)(phi - plo));
+            interp = !interp;
+            mid = min(max(mid, plo + 1u), phi - 1u);
+            const uint32_t v = __ldg(W + mid);
+            if (v >= C.x_c) {
+              plo = mid;
+              wlo = v;
+            } else {
+              phi = mid;
+              whi = v;
+            }
+          }
+          r.c = phi;
         }
-        r.c = phi;
       }
       const uint32_t cap = r.len < C.b_max ? r.len : C.b_max;
       const uint32_t bi = P.sm[C.off_bidx + cap];
@@ -687,7 +708,8 @@ __global__ void __launch_bounds__(TMA_NW * 32, 1) k1s_stream_tma(const uint8_t *
 // candidate m of the snapshot, one warp per clip-path snapshot.  Lane g < M
 // holds queue g's record; the warp walks the live windows [c_q, len_q) of the
 // snapshot's queues in rows of 32 consecutive waits (eight rows' loads in
-// flight; the next snapshot's windows prefetched into L2).  Waits are non-increasing from the head (checked, Q24), so a row
+// flight; an L2 prefetch of the next snapshot's windows was measured to add
+// 1.8 GB of DRAM reads per call for no time).  Waits are non-increasing from the head (checked, Q24), so a row
 // whose first wait is below every candidate's threshold min_m thr_m and which
 // lies past the queue's served head is below x_c - L_m for every m:
 // its G values go to one running sum T that every U_m receives.  Only the
@@ -732,16 +754,6 @@ __global__ void __launch_bounds__(256) k1s_clip(const uint8_t *__restrict__ gimg
   const int lane = threadIdx.x & 31;
   const int64_t wid = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  // the live windows of the warp's next snapshot are prefetched into L2 while
-  // this one is scored (the loop is latency-bound: one snapshot at a time)
-  auto prefetch_snap = [&](int64_t li) {
-    if (li >= n_slow || lane >= M) return;
-    const QRec *r = a.rec + a.slow_list[li] * M + lane;
-    const uint32_t len = r->len, c = r->c;
-    const char *p0 = reinterpret_cast<const char *>(a.waits + r->lo + c);
-    for (uint32_t b = 0; b < 4u * (len > c ? len - c : 0u); b += 128u) asm volatile("prefetch.global.L2 [%0];" ::"l"(p0 + b));
-  };
-  prefetch_snap(wid);
   for (int64_t li = wid; li < n_slow; li += nw) {  // warp-uniform
     const int64_t s = a.slow_list[li];
     const SmemCfg C = smem_cfg(P, a.cfg_idx ? (int)a.cfg_idx[s] : 0);  // < ncfg (k1s_prep)
@@ -755,7 +767,6 @@ __global__ void __launch_bounds__(256) k1s_clip(const uint8_t *__restrict__ gimg
       rB = r->B;
       if (rlen) rthr = r->thr;  // empty queue: no candidate (its sums are unused)
     }
-    prefetch_snap(li + nw);
     uint32_t thr[MM], K[MM];
     uint64_t U[MM];
 #pragma unroll
