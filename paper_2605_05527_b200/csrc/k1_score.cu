@@ -2,7 +2,7 @@
 // (Algorithm 1, on the system state of S:112-115).  Two mappings:
 //
 // k1_thread (Algorithm 1, short snapshots; the default below 1,024 waits per
-//   snapshot): one thread per snapshot for the per-queue logic, one balanced
+//   snapshot): a lane pair per snapshot for the per-queue logic, one balanced
 //   pass of the warp for the Eq. 3-4 sums (see the comment above it).
 // k1_score (warp segments): one segment of LPS lanes per snapshot
 //   (grid-stride), model g's queue owned by lane group g (decide.cuh); used
@@ -172,16 +172,17 @@ cudaError_t launch_lps(const uint8_t *img, const ImgLayout &lay, const ScoreArgs
 }
 
 // ---------------------------------------------------------------------------
-// Short snapshots under Algorithm 1: one THREAD per snapshot (k1_thread).
+// Short snapshots under Algorithm 1: one or two LANES per snapshot (k1_thread).
 // A warp segment spends warp-wide shuffles and reductions on a handful of
 // waits (harvested cfg3 states: 33 waits over 8 queues on average, median
-// queue 2), so here each lane owns a snapshot's decision logic:
+// queue 2), so here a lane (or a lane pair, each with half the queues) owns a
+// snapshot's decision logic:
 //   per queue q: Eq. 5 (bidx, Q8) and Eq. 6 (a count over the padded
 //   exit-minor latency row, Q2); S_q(m) = floor(H(L_m) (tot - srv_m) /
 //   2^28) and the Eq. 7 argmin (S, m) (Q3) -- the fast path of decide.cuh
 //   (same integers), valid when every head wait is below x_c - max L.
 // The sums come from one balanced pass of the whole warp: the waits of the
-// warp's 32 consecutive snapshots are one contiguous region, read as 16-byte
+// warp's 16 (32) consecutive snapshots are one contiguous region, read as 16-byte
 // vectors (8 waits per lane, 256 per trip) whatever the queue-length mix; G(w)
 // (Q5) of every wait with the SLO's tables (a warp whose snapshots mix SLOs
 // takes the per-lane loop below), an exclusive running sum E over the region
@@ -193,8 +194,6 @@ cudaError_t launch_lps(const uint8_t *img, const ImgLayout &lay, const ScoreArgs
 // A snapshot with a head at or past x_c - max L (some task may clip) is
 // appended to a list that the warp-segment kernel (k1_score, general clip
 // path) scores afterwards.
-constexpr int K1T_THREADS = 512;
-constexpr int K1T_WARPS = K1T_THREADS / 32;
 
 __device__ __forceinline__ uint32_t lds32(uint32_t a) {  // read-only tables / bitmap after a __syncwarp
   uint32_t v;
@@ -227,9 +226,15 @@ struct GSh {
   }
 };
 
-template <int MM>
-__global__ void __launch_bounds__(K1T_THREADS, 1) k1_thread(const uint8_t *__restrict__ gimg, ImgLayout lay,
-                                                           ScoreArgs a, uint32_t cap) {
+// LPN lanes per snapshot (1 or 2): lane h of a snapshot owns its queues
+// q = h HQ + j, j < HQ = MM / LPN; the snapshot's total, the Eq. 7 argmin and
+// the per-lane fallback combine over the LPN lanes with one xor-shuffle.
+template <int MM, int LPN, int NT>
+__global__ void __launch_bounds__(NT, 1) k1_thread(const uint8_t *__restrict__ gimg, ImgLayout lay, ScoreArgs a,
+                                                  uint32_t cap) {
+  constexpr int HQ = MM / LPN;       // queues per lane
+  constexpr int SPI = 32 / LPN;      // snapshots per warp iteration
+  constexpr int NW = NT / 32;
   extern __shared__ __align__(16) uint8_t smem[];
   __shared__ uint64_t mbar;
   stage_image(smem, gimg, a.stage_bytes, &mbar);
@@ -237,112 +242,116 @@ __global__ void __launch_bounds__(K1T_THREADS, 1) k1_thread(const uint8_t *__res
   if (a.stage_bytes < lay.bytes) P.hb = gimg;  // H tables stay in global memory (L1-cached)
   const int M = P.M;
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const int h = LPN == 1 ? 0 : (lane & (LPN - 1));  // this lane's half of the snapshot's queues
   const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(smem);
   // this warp's scratch: E [cap + 4] u64, then the queue-start bitmap [cap / 32]
   const uint32_t sE = sbase + ((a.stage_bytes + 127u) & ~127u) + (uint32_t)wib * (cap * 8u + 32u + cap / 8u);
   const uint32_t sBits = sE + cap * 8u + 32u;
-  const int64_t nwarps = (int64_t)gridDim.x * K1T_WARPS;
-  auto out_empty = [&](int64_t s, uint8_t flag) {
+  const int64_t nwarps = (int64_t)gridDim.x * NW;
+  auto out_empty = [&](int64_t s, uint8_t flag) {  // by lane h == 0
     a.m[s] = 0; a.e[s] = 0; a.B[s] = 0; a.L[s] = 0; a.S[s] = 0;
     a.flags[s] = flag;
     if (a.cand)
       for (int q = 0; q < M; ++q) a.cand[s * M + q] = ~0ull;
   };
-  // warps stride over groups of 32 snapshots (snapshot sizes are correlated
+  auto pair_or = [&](bool v) {  // whole warp (the shuffle is never skipped)
+    if (LPN == 1) return v;
+    const int o = __shfl_xor_sync(FULL, (int)v, 1);
+    return v || o != 0;
+  };
+  // warps stride over groups of SPI snapshots (snapshot sizes are correlated
   // along the batch: strided groups balance the warps); the next group's CSR
   // rows and SLO indices are prefetched into L2 at the start of a group, its
   // waits region once its bounds (loaded early) are known
-  const int64_t stride = nwarps * 32;
-  const int64_t wend = a.n;
-  for (int64_t s0 = ((int64_t)blockIdx.x * K1T_WARPS + wib) * 32; s0 < a.n; s0 += stride) {  // warp-uniform
-    const int64_t s = s0 + lane;
-    const bool live = s < wend;
+  const int64_t stride = nwarps * SPI;
+  for (int64_t s0 = ((int64_t)blockIdx.x * NW + wib) * SPI; s0 < a.n; s0 += stride) {  // warp-uniform
+    const int64_t s = s0 + lane / LPN;
+    const bool live = s < a.n;
     const int64_t s1 = s0 + stride;  // the next group
     uint64_t nb = 0ull;  // lane 0: its region start, lane 31: its region end
     if (s1 < a.n) {
       const char *nq = reinterpret_cast<const char *>(a.q_off + s1 * M);
-      if ((uint32_t)lane * 128u < 32u * 8u * (uint32_t)M + 8u) asm volatile("prefetch.global.L2 [%0];" ::"l"(nq + 128 * lane));
+      if ((uint32_t)lane * 128u < (uint32_t)SPI * 8u * (uint32_t)M + 8u)
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(nq + 128 * lane));
       if (lane == 30 && a.cfg_idx) asm volatile("prefetch.global.L2 [%0];" ::"l"(a.cfg_idx + s1));
       if (lane == 0) nb = __ldg(a.q_off + s1 * M);
-      if (lane == 31) nb = __ldg(a.q_off + min(s1 + 32, a.n) * M);
+      if (lane == 31) nb = __ldg(a.q_off + min(s1 + SPI, a.n) * M);
     }
     const int k = live ? (a.cfg_idx ? (int)a.cfg_idx[s] : 0) : 0;
     const bool cfg_ok = k < P.ncfg;
     const SmemCfg C = smem_cfg(P, cfg_ok ? k : 0);
-    // CSR row and head waits: all loads independent; offsets kept relative to
-    // the group's region start R0 (a region of 2^31 waits or more -- 8 GB for
-    // 32 snapshots -- goes to the warp segments whole)
-    uint32_t rel[MM + 1];
+    // this lane's CSR boundaries (queues h HQ .. h HQ + HQ, clamped to M) and
+    // head waits; offsets kept relative to the group's region start R0 (a
+    // region of 2^31 waits or more goes to the warp segments whole)
+    uint32_t rel[HQ + 1];
     uint64_t R0, R1;
     bool huge;
     {
-      uint64_t off[MM + 1];
+      uint64_t off[HQ + 1];
 #pragma unroll
-      for (int q = 0; q <= MM; ++q) off[q] = live && q <= M ? __ldg(a.q_off + s * M + q) : 0ull;
+      for (int j = 0; j <= HQ; ++j) off[j] = live ? __ldg(a.q_off + s * M + min(h * HQ + j, M)) : 0ull;
       R0 = __shfl_sync(FULL, off[0], 0);
-      const int ll = 31 - __clz(__ballot_sync(FULL, live));
-      R1 = 0ull;
-#pragma unroll
-      for (int q = 0; q <= MM; ++q)
-        if (q == M) R1 = __shfl_sync(FULL, off[q], ll);
+      const int ll = 31 - __clz(__ballot_sync(FULL, live));  // the last live snapshot's last lane
+      R1 = __shfl_sync(FULL, off[HQ], ll);
       huge = R1 - R0 >= (1ull << 31);
 #pragma unroll
-      for (int q = 0; q <= MM; ++q) rel[q] = live ? (uint32_t)(off[q] - R0) : 0u;
+      for (int j = 0; j <= HQ; ++j) rel[j] = live ? (uint32_t)(off[j] - R0) : 0u;
     }
-    uint32_t relM = 0u;  // rel[M]: this snapshot's end in the region
-#pragma unroll
-    for (int q = 0; q <= MM; ++q)
-      if (q == M) relM = rel[q];
     {  // L2 prefetch of the next group's waits region (its bounds loaded at the top)
       const uint64_t n0 = __shfl_sync(FULL, nb, 0), n1 = __shfl_sync(FULL, nb, 31);
       const char *nw = reinterpret_cast<const char *>(a.waits + n0);
       for (uint64_t b = 128u * (uint64_t)lane; b < 4u * (n1 - n0); b += 4096u) asm volatile("prefetch.global.L2 [%0];" ::"l"(nw + b));
     }
     const uint32_t *Wr = a.waits + R0;  // the region's waits
-    uint32_t pk[MM];  // e | bi << 4 | feasible << 12 | min(B*, len) << 16; 0xFFFFFFFF: empty queue
+    uint32_t pk[HQ];  // e | bi << 4 | feasible << 12 | min(B*, len) << 16; 0xFFFFFFFF: empty queue
     bool active = false;
     {
-      uint32_t head[MM];
+      uint32_t head[HQ];
       bool slow = false, any = false;
 #pragma unroll
-      for (int q = 0; q < MM; ++q) {
-        const bool has = q < M && rel[q + 1] > rel[q];
-        head[q] = has ? __ldg(Wr + rel[q]) : 0u;
-        slow |= has && head[q] >= C.fast_lim;
+      for (int j = 0; j < HQ; ++j) {
+        const bool has = rel[j + 1] > rel[j];
+        head[j] = has ? __ldg(Wr + rel[j]) : 0u;
+        slow |= has && head[j] >= C.fast_lim;
         any |= has;
       }
+      slow = pair_or(slow);
+      any = pair_or(any);
       if (live) {
         if (!cfg_ok) {
-          out_empty(s, ES_FLAG_BAD_INPUT);
-          if (atomicCAS(&a.dstat->code, 0u, (uint32_t)ES_ERR_ARG) == 0u) a.dstat->item = s;
+          if (h == 0) {
+            out_empty(s, ES_FLAG_BAD_INPUT);
+            if (atomicCAS(&a.dstat->code, 0u, (uint32_t)ES_ERR_ARG) == 0u) a.dstat->item = s;
+          }
         } else if (slow || huge) {  // some task may clip: the general path (k1_score on the list)
-          a.list[atomicAdd(a.list_n, 1ull)] = (uint32_t)s;
+          if (h == 0) a.list[atomicAdd(a.list_n, 1ull)] = (uint32_t)s;
         } else if (!any) {
-          out_empty(s, ES_FLAG_NO_WORK);
+          if (h == 0) out_empty(s, ES_FLAG_NO_WORK);
         } else {
           active = true;
         }
       }
-      // Eq. 5 / Eq. 6 of every queue
+      // Eq. 5 / Eq. 6 of this lane's queues
 #pragma unroll
-      for (int q = 0; q < MM; ++q) {
-        pk[q] = 0xFFFFFFFFu;
-        const uint32_t len = q < M ? rel[q + 1] - rel[q] : 0u;
+      for (int j = 0; j < HQ; ++j) {
+        pk[j] = 0xFFFFFFFFu;
+        const int q = h * HQ + j;
+        const uint32_t len = rel[j + 1] - rel[j];
         if (!active || !len) continue;
         const uint32_t cap_b = len < C.b_max ? len : C.b_max;
         const uint32_t bi = P.sm[C.off_bidx + cap_b];
         const uint32_t nsv = min((uint32_t)P.bs[bi], len);
         const uint32_t mbits = P.mask[q];
-        const unsigned bits = head[q] <= C.tau ? ((1u << eq6_count(P, q, bi, C.tau - head[q])) - 1u) & mbits : 0u;
+        const unsigned bits = head[j] <= C.tau ? ((1u << eq6_count(P, q, bi, C.tau - head[j])) - 1u) & mbits : 0u;
         const uint32_t e = bits ? 31u - __clz(bits) : (uint32_t)(__ffs(mbits) - 1);
-        pk[q] = e | (bi << 4) | (bits ? 0x1000u : 0u) | (nsv << 16);
+        pk[j] = e | (bi << 4) | (bits ? 0x1000u : 0u) | (nsv << 16);
       }
     }
     const unsigned b_act = __ballot_sync(FULL, active);
     if (b_act == 0u) continue;
-    uint64_t tot = 0ull, srv[MM];
+    uint64_t tot = 0ull, srv[HQ];  // tot: this lane's part of the snapshot total
 #pragma unroll
-    for (int q = 0; q < MM; ++q) srv[q] = 0ull;
+    for (int j = 0; j < HQ; ++j) srv[j] = 0ull;
     bool bad = false;
     // ---- the balanced pass: one SLO across the warp's active snapshots
     const int kf = __shfl_sync(FULL, k, __ffs(b_act) - 1);
@@ -357,15 +366,16 @@ __global__ void __launch_bounds__(K1T_THREADS, 1) k1_thread(const uint8_t *__res
       uint64_t carry = 0ull;
       uint32_t pcarry = 0xFFFFFFFFu;
       bool inv = false;
+      const uint32_t lo_x = rel[0] + mis, hi_x = rel[HQ] + mis;  // this lane's span of boundaries
       for (uint32_t cb = 0; cb < nrel; cb += cap) {  // warp-uniform chunks
         const uint32_t ce = min(cb + cap, nrel);
         for (uint32_t j = lane; j < cap / 32u; j += 32u) asm volatile("st.shared.u32 [%0], 0;" ::"r"(sBits + 4u * j));
         __syncwarp();
-        if (live && relM + mis >= cb && rel[0] + mis < ce) {  // queue starts of this chunk (no predecessor check, Q24)
+        if (live && hi_x >= cb && lo_x < ce) {  // queue starts of this chunk (no predecessor check, Q24)
 #pragma unroll
-          for (int q = 0; q < MM; ++q) {
-            const uint32_t x = rel[q] + mis;
-            if (q < M && x >= cb && x < ce)
+          for (int j = 0; j < HQ; ++j) {
+            const uint32_t x = rel[j] + mis;
+            if (h * HQ + j < M && x >= cb && x < ce)
               asm volatile("red.shared.or.b32 [%0], %1;" ::"r"(sBits + 4u * ((x - cb) >> 5)), "r"(1u << ((x - cb) & 31u)));
           }
         }
@@ -421,91 +431,109 @@ __global__ void __launch_bounds__(K1T_THREADS, 1) k1_thread(const uint8_t *__res
           carry += __shfl_sync(FULL, sc, 31);
         }
         __syncwarp();
-        if (active && relM + mis >= cb && rel[0] + mis < ce) {  // this lane's queue boundaries inside the chunk
+        if (active && hi_x >= cb && lo_x < ce) {  // this lane's queue boundaries inside the chunk
 #pragma unroll
-          for (int q = 0; q <= MM; ++q) {
-            if (q > M) continue;
-            const uint32_t x = rel[q] + mis;
-            if (x >= cb && x < ce) {
+          for (int j = 0; j <= HQ; ++j) {
+            const uint32_t x = rel[j] + mis;
+            const bool first = h == 0 && j == 0, last = h == LPN - 1 && j == HQ;  // the snapshot's start / end
+            const bool own = j < HQ && h * HQ + j < M;
+            if ((first || last || own) && x >= cb && x < ce) {
               const uint64_t e = lds64(sE + 8u * (x - cb));
-              if (q == 0) tot -= e;
-              if (q == M) tot += e;
-              if (q < M) srv[q] -= e;
+              if (first) tot -= e;
+              if (last) tot += e;
+              if (own) srv[j] -= e;
             }
-            if (q < M) {
-              const uint32_t x1 = x + (pk[q] >> 16);
-              if (x1 >= cb && x1 < ce) srv[q] += lds64(sE + 8u * (x1 - cb));
+            if (own) {
+              const uint32_t x1 = x + (pk[j] >> 16);
+              if (x1 >= cb && x1 < ce) srv[j] += lds64(sE + 8u * (x1 - cb));
             }
           }
         }
         __syncwarp();
       }
-      if (active && relM + mis == nrel) {  // boundaries at the region's end (the last lane): E = the final sum
+      if (active && hi_x == nrel) {  // boundaries at the region's end: E = the final sum
 #pragma unroll
-        for (int q = 0; q <= MM; ++q) {
-          if (q > M) continue;
-          const uint32_t x = rel[q] + mis;
+        for (int j = 0; j <= HQ; ++j) {
+          const uint32_t x = rel[j] + mis;
+          const bool first = h == 0 && j == 0, last = h == LPN - 1 && j == HQ;
+          const bool own = j < HQ && h * HQ + j < M;
           if (x == nrel) {
-            if (q == 0) tot -= carry;
-            if (q == M) tot += carry;
-            if (q < M) srv[q] -= carry;
+            if (first) tot -= carry;
+            if (last) tot += carry;
+            if (own) srv[j] -= carry;
           }
-          if (q < M && x + (pk[q] >> 16) == nrel) srv[q] += carry;
+          if (own && x + (pk[j] >> 16) == nrel) srv[j] += carry;
         }
       }
       flat = !__any_sync(FULL, inv);  // an inversion: redo the warp per lane (flags it exactly)
     }
-    if (!flat && active) {
+    if (!flat) {
       // ---- per-lane loop (mixed SLOs or an inversion in the region)
       tot = 0ull;
-      const GSh G{sbase + C.off_A, sbase + C.off_Bt, 4u * C.r, C.nA1};
+      if (active) {
+        const GSh G{sbase + C.off_A, sbase + C.off_Bt, 4u * C.r, C.nA1};
 #pragma unroll
-      for (int q = 0; q < MM; ++q) {
-        srv[q] = 0ull;
-        const uint32_t len = q < M ? rel[q + 1] - rel[q] : 0u;
-        if (!len) continue;
-        const uint32_t *W = Wr + rel[q];
-        uint32_t prev = __ldg(W);
-        uint64_t Q = G(prev), sv = Q;  // nsv >= 1
-        for (uint32_t p = 1; p < len; ++p) {
-          const uint32_t w = __ldg(W + p);
-          bad |= w > prev;
-          prev = w;
-          const uint64_t g = G(w);
-          Q += g;
-          if (p < (pk[q] >> 16)) sv += g;
+        for (int j = 0; j < HQ; ++j) {
+          srv[j] = 0ull;
+          const uint32_t len = rel[j + 1] - rel[j];
+          if (!len) continue;
+          const uint32_t *W = Wr + rel[j];
+          uint32_t prev = __ldg(W);
+          uint64_t Q = G(prev), sv = Q;  // nsv >= 1
+          for (uint32_t p = 1; p < len; ++p) {
+            const uint32_t w = __ldg(W + p);
+            bad |= w > prev;
+            prev = w;
+            const uint64_t g = G(w);
+            Q += g;
+            if (p < (pk[j] >> 16)) sv += g;
+          }
+          tot += Q;
+          srv[j] = sv;
         }
-        tot += Q;
-        srv[q] = sv;
+      }
+      bad = pair_or(bad);
+    }
+    if (LPN == 2) tot += __shfl_xor_sync(FULL, tot, 1);  // the snapshot's total over both halves
+    // Eq. 3-4 on each candidate's predicted state, Eq. 7 argmin (S, m)
+    uint64_t bS = ~0ull;
+    uint32_t bq = 0xFFu, bpk = 0u;
+    if (active && !bad) {
+      const uint64_t *Hq = reinterpret_cast<const uint64_t *>(P.hb + C.off_H);
+#pragma unroll
+      for (int j = 0; j < HQ; ++j) {
+        const int q = h * HQ + j;
+        if (q >= M) continue;
+        uint64_t Sv = ~0ull;
+        if (pk[j] != 0xFFFFFFFFu) {
+          const uint32_t e = pk[j] & 15u, bi = (pk[j] >> 4) & 0xFFu;
+          const uint64_t Hc = Hq[((size_t)q * P.E + e) * P.nb + bi];
+          const uint64_t H = Hc == ~0ull ? 0ull : Hc;  // L >= x_c: every task clips (k_build_tables)
+          const uint64_t u = tot - srv[j];
+          const uint64_t lo = H * u, hi = __umul64hi(H, u);
+          Sv = (hi << (64 - F)) | (lo >> F);
+          if (Sv < bS || bq == 0xFFu) {
+            bS = Sv;
+            bq = (uint32_t)q;
+            bpk = pk[j];
+          }
+        }
+        if (a.cand) a.cand[s * M + q] = Sv;
       }
     }
-    if (!active) continue;
+    if (LPN == 2) {  // (S, m) argmin over both halves (the partner's queues: higher m for h = 0)
+      const uint64_t oS = __shfl_xor_sync(FULL, bS, 1);
+      const uint32_t oq = __shfl_xor_sync(FULL, bq, 1), opk = __shfl_xor_sync(FULL, bpk, 1);
+      if (oq != 0xFFu && (bq == 0xFFu || oS < bS || (oS == bS && oq < bq))) {
+        bS = oS;
+        bq = oq;
+        bpk = opk;
+      }
+    }
+    if (!active || h != 0) continue;
     if (bad) {
       out_empty(s, ES_FLAG_BAD_INPUT);
       continue;
-    }
-    // Eq. 3-4 on each candidate's predicted state, Eq. 7 argmin (S, m)
-    const uint64_t *Hq = reinterpret_cast<const uint64_t *>(P.hb + C.off_H);
-    uint64_t bS = ~0ull;
-    uint32_t bq = 0u, bpk = 0u;
-#pragma unroll
-    for (int q = 0; q < MM; ++q) {
-      if (q >= M) continue;
-      uint64_t Sv = ~0ull;
-      if (pk[q] != 0xFFFFFFFFu) {
-        const uint32_t e = pk[q] & 15u, bi = (pk[q] >> 4) & 0xFFu;
-        const uint64_t Hc = Hq[((size_t)q * P.E + e) * P.nb + bi];
-        const uint64_t H = Hc == ~0ull ? 0ull : Hc;  // L >= x_c: every task clips (k_build_tables)
-        const uint64_t u = tot - srv[q];
-        const uint64_t lo = H * u, hi = __umul64hi(H, u);
-        Sv = (hi << (64 - F)) | (lo >> F);
-        if (Sv < bS || bS == ~0ull) {
-          bS = Sv;
-          bq = (uint32_t)q;
-          bpk = pk[q];
-        }
-      }
-      if (a.cand) a.cand[s * M + q] = Sv;
     }
     const uint32_t e = bpk & 15u, bi = (bpk >> 4) & 0xFFu;
     a.m[s] = (uint8_t)bq;
@@ -517,8 +545,8 @@ __global__ void __launch_bounds__(K1T_THREADS, 1) k1_thread(const uint8_t *__res
   }
 }
 
-template <int MM>
-cudaError_t launch_thread(const uint8_t *img, const ImgLayout &lay, ScoreArgs a, cudaStream_t st, int sms) {
+template <int MM, int LPN, int NT>
+cudaError_t launch_thread_t(const uint8_t *img, const ImgLayout &lay, ScoreArgs a, cudaStream_t st, int sms) {
   // the clip-path list (u32 indices) and its counter: stream-ordered scratch
   void *scratch = nullptr;
   const size_t list_bytes = ((size_t)a.n * sizeof(uint32_t) + 15u) & ~(size_t)15u;
@@ -527,30 +555,38 @@ cudaError_t launch_thread(const uint8_t *img, const ImgLayout &lay, ScoreArgs a,
   a.list = static_cast<uint32_t *>(scratch);
   a.list_n = reinterpret_cast<unsigned long long *>(static_cast<uint8_t *>(scratch) + list_bytes);
   e = cudaMemsetAsync(a.list_n, 0, sizeof(unsigned long long), st);
-  // one CTA of 16 warps per SM; what shared memory the staged image leaves
+  // one CTA of NT threads per SM; what shared memory the staged image leaves
   // becomes each warp's E chunk (cap positions, a multiple of 256)
+  constexpr int NW = NT / 32;
   int dev = 0, optin = 0;
   if (e == cudaSuccess) e = cudaGetDevice(&dev);
   if (e == cudaSuccess) e = cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
   const size_t img_b = ((size_t)a.stage_bytes + 127u) & ~(size_t)127u;
   const int64_t room = (int64_t)optin - (int64_t)img_b - 256;
-  int64_t capw = room / K1T_WARPS;  // bytes per warp: cap * 8 + 32 + cap / 8
+  int64_t capw = room / NW;  // bytes per warp: cap * 8 + 32 + cap / 8
   uint32_t cap = (uint32_t)std::min<int64_t>(std::max<int64_t>((capw - 32) * 8 / 65, 0) & ~255ll, 4096);
   if (e == cudaSuccess && cap < 256u) e = cudaErrorInvalidConfiguration;
-  const size_t dyn = img_b + (size_t)K1T_WARPS * (cap * 8u + 32u + cap / 8u);
-  auto kern = k1_thread<MM>;
+  const size_t dyn = img_b + (size_t)NW * (cap * 8u + 32u + cap / 8u);
+  auto kern = k1_thread<MM, LPN, NT>;
   if (e == cudaSuccess) e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
   if (e == cudaSuccess) {
-    int64_t blocks = (a.n + K1T_THREADS - 1) / K1T_THREADS;
+    int64_t blocks = (a.n * LPN + NT - 1) / NT;
     if (blocks > sms) blocks = sms;
     if (blocks < 1) blocks = 1;
-    kern<<<(unsigned)blocks, K1T_THREADS, dyn, st>>>(img, lay, a, cap);
+    kern<<<(unsigned)blocks, NT, dyn, st>>>(img, lay, a, cap);
     e = cudaGetLastError();
   }
   // the listed (clip-path) snapshots: the warp-segment kernel, general path
   if (e == cudaSuccess) e = launch_t<16, MM>(img, lay, a, st, sms);
   const cudaError_t f = cudaFreeAsync(scratch, st);
   return e != cudaSuccess ? e : f;
+}
+
+// two lanes per snapshot, 16 warps per SM (measured on the harvested cfg3
+// batch: 1.36 ms; one lane per snapshot 1.42 ms; two lanes at 24 warps 1.39 ms)
+template <int MM>
+cudaError_t launch_thread(const uint8_t *img, const ImgLayout &lay, ScoreArgs a, cudaStream_t st, int sms) {
+  return launch_thread_t<MM, 2, 512>(img, lay, a, st, sms);
 }
 
 }  // namespace
