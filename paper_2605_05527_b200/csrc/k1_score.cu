@@ -254,10 +254,11 @@ __global__ void __launch_bounds__(NT, 1) k1_thread(const uint8_t *__restrict__ g
     if (a.cand)
       for (int q = 0; q < M; ++q) a.cand[s * M + q] = ~0ull;
   };
-  auto pair_or = [&](bool v) {  // whole warp (the shuffle is never skipped)
-    if (LPN == 1) return v;
-    const int o = __shfl_xor_sync(FULL, (int)v, 1);
-    return v || o != 0;
+  auto pair_or = [&](bool v) {  // OR over the snapshot's LPN lanes; whole warp (no shuffle is skipped)
+    int x = v ? 1 : 0;
+#pragma unroll
+    for (int o = 1; o < LPN; o <<= 1) x |= __shfl_xor_sync(FULL, x, o);
+    return x != 0;
   };
   // warps stride over groups of SPI snapshots (snapshot sizes are correlated
   // along the batch: strided groups balance the warps); the next group's CSR
@@ -494,7 +495,8 @@ __global__ void __launch_bounds__(NT, 1) k1_thread(const uint8_t *__restrict__ g
       }
       bad = pair_or(bad);
     }
-    if (LPN == 2) tot += __shfl_xor_sync(FULL, tot, 1);  // the snapshot's total over both halves
+#pragma unroll
+    for (int o = 1; o < LPN; o <<= 1) tot += __shfl_xor_sync(FULL, tot, o);  // the snapshot's total over its lanes
     // Eq. 3-4 on each candidate's predicted state, Eq. 7 argmin (S, m)
     uint64_t bS = ~0ull;
     uint32_t bq = 0xFFu, bpk = 0u;
@@ -521,9 +523,10 @@ __global__ void __launch_bounds__(NT, 1) k1_thread(const uint8_t *__restrict__ g
         if (a.cand) a.cand[s * M + q] = Sv;
       }
     }
-    if (LPN == 2) {  // (S, m) argmin over both halves (the partner's queues: higher m for h = 0)
-      const uint64_t oS = __shfl_xor_sync(FULL, bS, 1);
-      const uint32_t oq = __shfl_xor_sync(FULL, bq, 1), opk = __shfl_xor_sync(FULL, bpk, 1);
+#pragma unroll
+    for (int o = 1; o < LPN; o <<= 1) {  // (S, m) argmin over the snapshot's lanes (lowest m on ties, Q3)
+      const uint64_t oS = __shfl_xor_sync(FULL, bS, o);
+      const uint32_t oq = __shfl_xor_sync(FULL, bq, o), opk = __shfl_xor_sync(FULL, bpk, o);
       if (oq != 0xFFu && (bq == 0xFFu || oS < bS || (oS == bS && oq < bq))) {
         bS = oS;
         bq = oq;
@@ -583,7 +586,8 @@ cudaError_t launch_thread_t(const uint8_t *img, const ImgLayout &lay, ScoreArgs 
 }
 
 // two lanes per snapshot, 16 warps per SM (measured on the harvested cfg3
-// batch: 1.36 ms; one lane per snapshot 1.42 ms; two lanes at 24 warps 1.39 ms)
+// batch: 1.36 ms; one lane per snapshot 1.42 ms; two lanes at 24 warps 1.39 ms;
+// four lanes 1.60 ms at 16 warps, 1.40 ms at 24)
 template <int MM>
 cudaError_t launch_thread(const uint8_t *img, const ImgLayout &lay, ScoreArgs a, cudaStream_t st, int sms) {
   return launch_thread_t<MM, 2, 512>(img, lay, a, st, sms);
