@@ -2,11 +2,12 @@
 // (steps a9, a10).
 //
 // P95 (reading Q15): the k-th smallest post-warmup latency, k = ceil(0.95 N),
-// found by exact radix selection with 12-bit digits.  Per scenario (one CTA):
-// the latencies are staged in shared memory when they fit (else re-read from
-// global), the top significant 12 bits form the first digit (so the first
-// histogram is spread, not piled into bin 0), and 1-3 histogram passes select
-// the exact value.
+// found by exact radix selection with 12-bit digits.  Per scenario (one CTA,
+// six per SM): the latencies are streamed from global memory with 16-byte
+// loads, a coarse histogram of min(T >> 12, 4095) selects the 4.096 ms bin of
+// the rank, and a second pass (an L2 re-read) histograms T & 0xFFF inside it
+// -> the exact value.  Ranks among T >= 16.77 s take a radix select from the
+// top significant bit instead (1-3 more passes).
 //
 // Groups (sweep points) use digits that are the same on every rank, so that
 // histograms from any number of ranks can be summed (all_reduce) before each
@@ -47,8 +48,24 @@ __device__ uint32_t find_bin(const T *hist, int nbins, uint64_t k, uint64_t *bef
   const int per = (nbins + NT - 1) / NT;
   const int b0 = threadIdx.x * per;
   uint64_t loc = 0;
-  for (int i = 0; i < per; ++i)
-    if (b0 + i < nbins) loc += (uint64_t)hist[b0 + i];
+  if constexpr (sizeof(T) == 4) {
+    if (nbins == 16 * NT) {  // full 4096-bin histogram (16-byte aligned): 4 x 16-byte loads, 4-way instead of 16-way conflicts
+      const uint4 *h4 = reinterpret_cast<const uint4 *>(hist + b0);
+      uint32_t l32 = 0;
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const uint4 x = h4[i];
+        l32 += x.x + x.y + x.z + x.w;
+      }
+      loc = l32;  // a CTA histogram of < 2^32 values
+    } else {
+      for (int i = 0; i < per; ++i)
+        if (b0 + i < nbins) loc += (uint64_t)hist[b0 + i];
+    }
+  } else {
+    for (int i = 0; i < per; ++i)
+      if (b0 + i < nbins) loc += (uint64_t)hist[b0 + i];
+  }
   // inclusive scan: warp shuffles, then the warp totals
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   uint64_t incl = loc;
@@ -82,6 +99,33 @@ __device__ uint32_t find_bin(const T *hist, int nbins, uint64_t k, uint64_t *bef
   return b;
 }
 
+// apply f to each of the n words at g (global): 16-byte loads of the aligned
+// interior, U per thread in flight, the (<= 3 + 3) edge words loaded singly
+template <int U, typename F>
+__device__ __forceinline__ void each_value(const uint32_t *g, uint32_t n, bool last_use, F f) {
+  const uint32_t off = (uint32_t)(((uintptr_t)g >> 2) & 3u);
+  const uint32_t lead = off ? min(4u - off, n) : 0u;
+  const uint4 *q4 = reinterpret_cast<const uint4 *>(g + lead);
+  const uint32_t nq = (n - lead) / 4u;
+  const uint32_t tail0 = lead + 4u * nq;
+  if (threadIdx.x < lead) f(__ldg(g + threadIdx.x));
+  if (threadIdx.x >= 8u && threadIdx.x - 8u < n - tail0) f(__ldg(g + tail0 + (threadIdx.x - 8u)));
+  for (uint32_t q = threadIdx.x; q < nq; q += U * NT) {
+    uint4 x[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+      if (q + u * NT < nq) x[u] = last_use ? __ldcs(q4 + q + u * NT) : __ldg(q4 + q + u * NT);
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+      if (q + u * NT < nq) {
+        f(x[u].x);
+        f(x[u].y);
+        f(x[u].z);
+        f(x[u].w);
+      }
+  }
+}
+
 struct StatsArgs {
   int64_t n_scen;
   int M;
@@ -92,124 +136,87 @@ struct StatsArgs {
   const uint64_t *stats;
   uint32_t *p95;  // per-scenario P95 or NULL
   const CfgRec *cfg;  // global copy of the records
-  uint32_t cap;       // values staged in shared memory when n <= cap
   uint32_t n_groups;  // 0: no group outputs
   uint64_t *counts;   // [G][ES_NGSTAT]
   uint64_t *hist0;    // [G][4096] coarse level
 };
 
-__global__ void __launch_bounds__(NT) k3_stats(StatsArgs a) {
-  __shared__ uint32_t hist[BINS];
+// shared layout of k3_stats: hist[4096] then priv[PRIV][32] -- the coarse bins
+// below PRIV (T < 131 ms: 99.9 % of cfg3's latencies) counted per lane, so a
+// warp's increments land in 32 distinct banks instead of piling onto the few
+// addresses the coarse histogram concentrates them on (same-address atomics
+// serialise: 129 M bank conflicts in the capture before this layout)
+constexpr uint32_t PRIV = 32;
+
+template <int U, int MINB>
+__global__ void __launch_bounds__(NT, MINB) k3_stats(StatsArgs a) {
+  __shared__ __align__(16) uint32_t hist[BINS + PRIV * 32];
+  uint32_t *priv = hist + BINS;
   __shared__ uint32_t s_max;
-  extern __shared__ __align__(16) uint32_t vals[];
-  __shared__ uint64_t mbar;
-  const uint32_t mb = (uint32_t)__cvta_generic_to_shared(&mbar);
-  uint32_t phase = 0;
-  if (threadIdx.x == 0) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(mb));
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
+  for (int i = threadIdx.x; i < BINS + (int)PRIV * 32; i += NT) hist[i] = 0u;
+  // per-scenario metadata, fetched one scenario ahead: its chain of global
+  // loads (status, config, group, trace span, the group columns) is in flight
+  // during the previous scenario's histogram passes
+  static_assert(ES_ST_INFEASIBLE == 5 && ES_ST_EXIT0 == ES_ST_ACC_BP + 1 && ES_ST_EXIT7 + 1 == ES_NSTAT, "cols");
+  // group column t -> scenario column: decisions .. infeasible, sum_lat, acc_bp, exit0 .. exit7
+  const int tcol = threadIdx.x < 6 ? (int)threadIdx.x : threadIdx.x == 6 ? ES_ST_SUM_LAT : ES_ST_ACC_BP + ((int)threadIdx.x - 7);
+  struct Meta {
+    uint64_t status, base, end, col;
+    uint32_t k, g;
+  };
+  auto fetch = [&](int64_t s, Meta &m) {
+    if (s >= a.n_scen) return;
+    const uint64_t *st = a.stats + s * ES_NSTAT;
+    m.status = st[ES_ST_STATUS];
+    m.k = a.cfg_idx ? (uint32_t)a.cfg_idx[s] : 0u;
+    m.g = a.group_id ? a.group_id[s] : 0u;
+    m.base = a.arr_off[s * a.M];
+    m.end = a.arr_off[s * a.M + a.M];
+    m.col = threadIdx.x < ES_NGSTAT ? st[tcol] : 0ull;
+  };
+  Meta nxt;
+  fetch(blockIdx.x, nxt);
+  const uint32_t lane = threadIdx.x & 31u, wid = threadIdx.x >> 5;
   __syncthreads();
   for (int64_t s = blockIdx.x; s < a.n_scen; s += gridDim.x) {
-    const uint64_t *st = a.stats + s * ES_NSTAT;
-    const int k = a.cfg_idx ? (int)a.cfg_idx[s] : 0;
-    if (st[ES_ST_STATUS] != 0ull) {
+    const Meta m = nxt;
+    fetch(s + gridDim.x, nxt);  // consumed on the next trip
+    if (m.status != 0ull) {
       if (a.p95 && threadIdx.x == 0) a.p95[s] = 0u;
       continue;
     }
-    const uint32_t g = a.group_id ? a.group_id[s] : 0u;
+    const uint32_t g = m.g;
     const bool grp = a.n_groups && g < a.n_groups;
-    if (grp && threadIdx.x < ES_NGSTAT) {
-      // group column -> scenario column: decisions .. infeasible, sum_lat, acc_bp, exit0 .. exit7
-      static_assert(ES_ST_INFEASIBLE == 5 && ES_ST_EXIT0 == ES_ST_ACC_BP + 1 && ES_ST_EXIT7 + 1 == ES_NSTAT, "cols");
-      const int t = (int)threadIdx.x;
-      const int col = t < 6 ? t : t == 6 ? ES_ST_SUM_LAT : ES_ST_ACC_BP + (t - 7);
+    if (grp && threadIdx.x < ES_NGSTAT)
       atomicAdd(reinterpret_cast<unsigned long long *>(a.counts + (uint64_t)g * ES_NGSTAT + threadIdx.x),
-                (unsigned long long)st[col]);
-    }
-    const uint32_t W = a.cfg[k].warmup;
-    const uint64_t base = a.arr_off[s * a.M];
-    const uint64_t total = a.arr_off[s * a.M + a.M] - base;
+                (unsigned long long)m.col);
+    const uint32_t W = a.cfg[m.k].warmup;
+    const uint64_t total = m.end - m.base;
     const uint32_t n = total > W ? (uint32_t)(total - W) : 0u;
     if (n == 0u) {
       if (a.p95 && threadIdx.x == 0) a.p95[s] = 0u;
       continue;
     }
-    const uint32_t *gsrc = a.lat + base + W;
-    const bool staged = n + 3u <= a.cap;  // + up to 3 leading words of 16-byte alignment
-    // stage the scenario's latencies into shared memory with TMA: one bulk copy
-    // of the 16-byte aligned span [gsrc - off, ...) (off <= 3 leading words
-    // ignored), the <= 3 trailing words loaded directly
-    const uint32_t *src = gsrc;
-    uint32_t off = 0u;  // staged: vals[off + i] holds latency i (vals 16-byte aligned)
-    if (staged) {
-      off = (uint32_t)(((uintptr_t)gsrc >> 2) & 3u);
-      const uint32_t nv4 = (n + off) / 4u;
-      if (threadIdx.x == 0 && nv4) {
-        // the previous scenario's generic-proxy reads of vals precede these async writes
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(mb), "r"(16u * nv4) : "memory");
-        const uint32_t dst = (uint32_t)__cvta_generic_to_shared(vals);
-        const uint8_t *gs = reinterpret_cast<const uint8_t *>(gsrc - off);
-        for (uint32_t o = 0; o < 16u * nv4; o += 16384u)
-          asm volatile(
-              "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                  dst + o),
-              "l"(gs + o), "r"(min(16384u, 16u * nv4 - o)), "r"(mb)
-              : "memory");
-      }
-      for (uint32_t j = 4u * nv4 + threadIdx.x; j < n + off; j += NT) vals[j] = gsrc[j - off];
-      if (nv4) {
-        uint32_t done = 0;
-        while (!done)
-          asm volatile(
-              "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
-              "selp.u32 %0, 1, 0, p;\n\t}"
-              : "=r"(done)
-              : "r"(mb), "r"(phase)
-              : "memory");
-        phase ^= 1u;
-      }
-      src = vals + off;
-    }
+    // the latencies are streamed from global memory twice (pass B hits L2:
+    // the scenario was read a moment before); hist is all zero here
+    const uint32_t *gsrc = a.lat + m.base + W;
+    if (threadIdx.x == 0) s_max = 0u;
     // pass A: coarse histogram min(T >> 12, 4095) -- the group level-0 digit,
     // and the first digit of the scenario's own selection
-    for (int i = threadIdx.x; i < BINS; i += NT) hist[i] = 0u;
-    if (threadIdx.x == 0) s_max = 0u;
-    __syncthreads();  // staged tail words and the zeroed histogram are visible
     uint32_t mx = 0;
-    // staged: 16-byte shared loads; the quads strictly inside [off, n + off)
-    // take no per-element test, the (at most two) edge quads do
-    const uint4 *v4 = reinterpret_cast<const uint4 *>(vals);
-    const uint32_t nq = (n + off + 3u) / 4u;
-    // (warp-aggregated updates -- __match_any, or a ballot loop per distinct
-    // bin -- measured 1.5x and 5.6x slower than plain shared atomics here)
-    auto add_bin = [&](uint32_t bin) {  // bin = 0xFFFFFFFF: no value
-      if (bin != 0xFFFFFFFFu) atomicAdd(&hist[bin], 1u);
-    };
-    if (staged) {
-      for (uint32_t q0 = threadIdx.x & ~31u; q0 < nq; q0 += NT) {  // warp-uniform trip count
-        const uint32_t q = q0 + (threadIdx.x & 31);
-        const uint4 x = q < nq ? v4[q] : make_uint4(0u, 0u, 0u, 0u);
-        const uint32_t j = 4u * q;
-        const uint32_t e[4] = {x.x, x.y, x.z, x.w};
-#pragma unroll
-        for (int c = 0; c < 4; ++c) {
-          const bool in = q < nq && j + c >= off && j + c < n + off;
-          if (in) mx = max(mx, e[c]);
-          add_bin(in ? min(e[c] >> 12, COARSE_OVF) : 0xFFFFFFFFu);
-        }
-      }
-    } else {
-      for (uint32_t i0 = threadIdx.x & ~31u; i0 < n; i0 += NT) {
-        const uint32_t i = i0 + (threadIdx.x & 31);
-        const uint32_t v = i < n ? __ldg(gsrc + i) : 0u;
-        if (i < n) mx = max(mx, v);
-        add_bin(i < n ? min(v >> 12, COARSE_OVF) : 0xFFFFFFFFu);
-      }
-    }
+    each_value<U>(gsrc, n, false, [&](uint32_t v) {
+      mx = max(mx, v);
+      const uint32_t b = min(v >> 12, COARSE_OVF);
+      atomicAdd(b < PRIV ? priv + b * 32u + lane : hist + b, 1u);
+    });
     mx = __reduce_max_sync(0xffffffffu, mx);
-    if ((threadIdx.x & 31) == 0) atomicMax(&s_max, mx);
+    __syncthreads();
+    if (lane == 0) atomicMax(&s_max, mx);
+    for (uint32_t b = wid; b < PRIV; b += NW) {  // fold the per-lane counts into hist
+      const uint32_t c = __reduce_add_sync(0xffffffffu, priv[b * 32u + lane]);
+      priv[b * 32u + lane] = 0u;
+      if (lane == 0) hist[b] += c;
+    }
     __syncthreads();
     const uint32_t vmax = s_max;
     const uint32_t top = min(vmax >> 12, COARSE_OVF);
@@ -223,33 +230,15 @@ __global__ void __launch_bounds__(NT) k3_stats(StatsArgs a) {
       uint64_t before;
       const uint32_t cb = find_bin(hist, (int)top + 1, kk, &before);  // syncs: flush reads done
       uint32_t res;
+      for (uint32_t i = threadIdx.x; i <= top; i += NT) hist[i] = 0u;
+      __syncthreads();
       if (cb < COARSE_OVF) {  // pass B: T & 0xFFF inside the coarse bin -> exact value
         kk -= before;
-        for (int i = threadIdx.x; i < BINS; i += NT) hist[i] = 0u;
-        __syncthreads();
-        if (staged) {
-          for (uint32_t q = threadIdx.x; q < nq; q += NT) {
-            const uint4 x = v4[q];
-            const uint32_t j = 4u * q;
-            // words outside [off, n + off) never match (masked to all ones)
-            const uint32_t e0 = j >= off && j < n + off ? x.x : 0xFFFFFFFFu;
-            const uint32_t e1 = j + 1u >= off && j + 1u < n + off ? x.y : 0xFFFFFFFFu;
-            const uint32_t e2 = j + 2u >= off && j + 2u < n + off ? x.z : 0xFFFFFFFFu;
-            const uint32_t e3 = j + 3u < n + off ? x.w : 0xFFFFFFFFu;
-            const bool h0 = (e0 >> 12) == cb, h1 = (e1 >> 12) == cb, h2 = (e2 >> 12) == cb, h3 = (e3 >> 12) == cb;
-            if (h0 | h1 | h2 | h3) {
-              if (h0) atomicAdd(&hist[e0 & 0xFFFu], 1u);
-              if (h1) atomicAdd(&hist[e1 & 0xFFFu], 1u);
-              if (h2) atomicAdd(&hist[e2 & 0xFFFu], 1u);
-              if (h3) atomicAdd(&hist[e3 & 0xFFFu], 1u);
-            }
-          }
-        } else {
-          for (uint32_t i = threadIdx.x; i < n; i += NT) {
-            const uint32_t v = __ldg(gsrc + i);
-            if ((v >> 12) == cb) atomicAdd(&hist[v & 0xFFFu], 1u);
-          }
-        }
+        const uint32_t key = cb << 12;
+        each_value<U>(gsrc, n, true, [&](uint32_t v) {
+          const uint32_t d = v ^ key;
+          if (d < 4096u) atomicAdd(&hist[d], 1u);
+        });
         __syncthreads();
         const uint32_t fb = find_bin(hist, BINS, kk, &before);
         res = (cb << 12) | fb;
@@ -264,7 +253,7 @@ __global__ void __launch_bounds__(NT) k3_stats(StatsArgs a) {
           __syncthreads();
           const uint32_t dmask = nb - 1u;
           for (uint32_t i = threadIdx.x; i < n; i += NT) {
-            const uint32_t v = src[i];
+            const uint32_t v = __ldg(gsrc + i);
             if (((uint64_t)v >> prev) == hv) atomicAdd(&hist[(v >> shift) & dmask], 1u);
           }
           __syncthreads();
@@ -278,6 +267,10 @@ __global__ void __launch_bounds__(NT) k3_stats(StatsArgs a) {
         res = (uint32_t)hv;
       }
       if (threadIdx.x == 0) a.p95[s] = res;
+      for (int i = threadIdx.x; i < BINS; i += NT) hist[i] = 0u;  // find_bin's reads are done
+    } else {
+      __syncthreads();  // flush reads done
+      for (uint32_t i = threadIdx.x; i <= top; i += NT) hist[i] = 0u;
     }
     __syncthreads();
   }
@@ -324,8 +317,16 @@ __device__ __forceinline__ bool level_digit(uint32_t v, int level, bool ovf, uin
 // CTA streams a contiguous run of them -- 16-byte loads of the latencies --
 // into one shared-memory histogram that is flushed to the group's global
 // histogram only when the run moves to another group (or ends).
-__global__ void __launch_bounds__(NT) k_group_level(GroupArgs a, const uint32_t *order, int64_t per_cta) {
+__global__ void __launch_bounds__(NT, 6) k_group_level(GroupArgs a, const uint32_t *order, int64_t per_cta) {
   __shared__ uint32_t hist[BINS];
+  {  // nothing to do at this level (levels 2-3 when no group's rank lies among T >= 16.77 s)
+    int need = 0;
+    for (uint32_t g = threadIdx.x; g < a.n_groups; g += NT) {
+      const uint64_t w1 = a.state[2 * g + 1];
+      need |= !(w1 & DONE) && w1 != 0ull && (a.level == 1 || (a.state[2 * g] & MODE_OVF));
+    }
+    if (!__syncthreads_or(need)) return;
+  }
   for (int i = threadIdx.x; i < BINS; i += NT) hist[i] = 0u;
   __syncthreads();
   const int64_t lo = (int64_t)blockIdx.x * per_cta, hi = ::min(lo + per_cta, a.n_scen);
@@ -344,11 +345,29 @@ __global__ void __launch_bounds__(NT) k_group_level(GroupArgs a, const uint32_t 
     dirty = false;
     __syncthreads();
   };
+  // per-scenario records fetched one scenario ahead (the scenario index two
+  // ahead), so the chain order -> stats / group / span is in flight during the
+  // previous scenario's stream; the group state and config are small tables
+  struct Meta {
+    uint64_t status, base, end;
+    uint32_t g, k;
+  };
+  auto fetch = [&](int64_t s, Meta &m) {
+    m.status = a.stats[s * ES_NSTAT + ES_ST_STATUS];
+    m.g = a.group_id ? a.group_id[s] : 0u;
+    m.k = a.cfg_idx ? (uint32_t)a.cfg_idx[s] : 0u;
+    m.base = a.arr_off[s * a.M];
+    m.end = a.arr_off[s * a.M + a.M];
+  };
+  Meta nxt{};
+  if (lo < hi) fetch(order[lo], nxt);
+  int64_t s_next = lo + 1 < hi ? (int64_t)order[lo + 1] : 0;
   for (int64_t j = lo; j < hi; ++j) {
-    const int64_t s = order[j];
-    const uint64_t *st = a.stats + s * ES_NSTAT;
-    if (st[ES_ST_STATUS] != 0ull) continue;
-    const uint32_t g = a.group_id ? a.group_id[s] : 0u;
+    const Meta m = nxt;
+    if (j + 1 < hi) fetch(s_next, nxt);
+    if (j + 2 < hi) s_next = order[j + 2];
+    if (m.status != 0ull) continue;
+    const uint32_t g = m.g;
     if (g >= a.n_groups) continue;
     const uint64_t w1 = a.state[2 * g + 1];
     if ((w1 & DONE) || w1 == 0ull) continue;  // resolved or empty group
@@ -356,33 +375,21 @@ __global__ void __launch_bounds__(NT) k_group_level(GroupArgs a, const uint32_t 
     const bool ovf = (w0 & MODE_OVF) != 0ull;
     if (!ovf && a.level != 1) continue;
     const uint32_t prefix = (uint32_t)w0;
-    const int k = a.cfg_idx ? (int)a.cfg_idx[s] : 0;
-    const uint32_t W = a.cfg[k].warmup;
-    const uint64_t base = a.arr_off[s * a.M];
-    const uint64_t total = a.arr_off[s * a.M + a.M] - base;
+    const uint32_t W = a.cfg[m.k].warmup;
+    const uint64_t base = m.base;
+    const uint64_t total = m.end - base;
     if (total <= W) continue;
     if (g != cur) {  // uniform across the CTA
       flush();
       cur = g;
     }
     dirty = true;
-    // latencies [b0, b1): scalar head up to 16-byte alignment, uint4 body, scalar tail
-    const uint64_t b0 = base + W, b1 = base + total;
-    const uint64_t h1 = ::min((uint64_t)((b0 + 3u) & ~3ull), b1), t0 = ::max((uint64_t)(b1 & ~3ull), h1);
-    uint32_t bin;
-    if (threadIdx.x < h1 - b0 && level_digit(a.lat[b0 + threadIdx.x], a.level, ovf, prefix, bin))
-      atomicAdd(&hist[bin], 1u);
-    if (threadIdx.x < b1 - t0 && level_digit(a.lat[t0 + threadIdx.x], a.level, ovf, prefix, bin))
-      atomicAdd(&hist[bin], 1u);
-    const uint4 *body = reinterpret_cast<const uint4 *>(a.lat + h1);
-    const uint64_t nv = (t0 - h1) / 4u;
-    for (uint64_t i = threadIdx.x; i < nv; i += NT) {
-      const uint4 q = __ldcs(body + i);  // streamed once per level: do not keep it in L1/L2
-      if (level_digit(q.x, a.level, ovf, prefix, bin)) atomicAdd(&hist[bin], 1u);
-      if (level_digit(q.y, a.level, ovf, prefix, bin)) atomicAdd(&hist[bin], 1u);
-      if (level_digit(q.z, a.level, ovf, prefix, bin)) atomicAdd(&hist[bin], 1u);
-      if (level_digit(q.w, a.level, ovf, prefix, bin)) atomicAdd(&hist[bin], 1u);
-    }
+    // latencies [base + W, base + total), streamed once per level (evict-first)
+    const int lvl = a.level;
+    each_value<2>(a.lat + base + W, (uint32_t)(total - W), true, [&](uint32_t v) {
+      uint32_t bin;
+      if (level_digit(v, lvl, ovf, prefix, bin)) atomicAdd(&hist[bin], 1u);
+    });
   }
   flush();
 }
@@ -491,24 +498,26 @@ StatsArgs stats_args(const uint8_t *img, const ImgLayout &lay, const es_traces &
   a.stats = out.scen_stats;
   a.p95 = out.scen_p95_us;
   a.cfg = reinterpret_cast<const CfgRec *>(img + lay.off_cfg);
-  a.cap = 12288;  // 48 KB of staged latencies per CTA
   return a;
 }
 
-cudaError_t launch_stats(const StatsArgs &a, cudaStream_t st, int sms) {
-  const size_t dyn = (size_t)a.cap * sizeof(uint32_t);
-  cudaError_t e = cudaFuncSetAttribute(k3_stats, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
-  if (e != cudaSuccess) return e;
+template <int U, int MINB>
+cudaError_t launch_stats_t(const StatsArgs &a, cudaStream_t st, int sms) {
   int occ = 0;
-  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k3_stats, NT, dyn);
+  cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k3_stats<U, MINB>, NT, 0);
   if (e != cudaSuccess) return e;
   int64_t blocks = a.n_scen;
   const int64_t cap = (int64_t)sms * (occ > 0 ? occ : 1) * 4;
   if (blocks > cap) blocks = cap;
   if (blocks < 1) blocks = 1;
-  k3_stats<<<(unsigned)blocks, NT, dyn, st>>>(a);
+  k3_stats<U, MINB><<<(unsigned)blocks, NT, 0, st>>>(a);
   return cudaGetLastError();
 }
+
+// two 16-byte loads in flight per thread, six CTAs (48 warps) per SM: measured
+// on cfg3 1.34 ms; four loads at five or four CTAs 1.42 / 1.49 ms, eight at
+// three 1.77 ms (the per-scenario selection steps, not the load depth, bound it)
+cudaError_t launch_stats(const StatsArgs &a, cudaStream_t st, int sms) { return launch_stats_t<2, 6>(a, st, sms); }
 
 }  // namespace
 
@@ -573,7 +582,9 @@ cudaError_t launch_group_hist(const uint8_t *img, const ImgLayout &lay, const es
     k_group_count<<<blocks, 256, 0, st>>>(tr.n_scen, tr.group_id, n_groups, cnt);
     k_group_scan<<<1, NT, 0, st>>>((uint32_t)nb, cnt);
     k_group_scatter<<<blocks, 256, 0, st>>>(tr.n_scen, tr.group_id, n_groups, cnt, order);
-    const int64_t ctas = std::min<int64_t>(tr.n_scen, (int64_t)sms * 8);
+    int occ = 0;  // one wave of resident CTAs, each a contiguous run of grouped scenarios
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_group_level, NT, 0);
+    const int64_t ctas = std::min<int64_t>(tr.n_scen, (int64_t)sms * std::max(occ, 1));
     const int64_t per = (tr.n_scen + ctas - 1) / ctas;
     k_group_level<<<(unsigned)((tr.n_scen + per - 1) / per), NT, 0, st>>>(a, order, per);
     e = cudaGetLastError();
