@@ -912,3 +912,53 @@ def test_full_size_cfg3_bench_config_sampled():
         k = (95 * v.size + 99) // 100
         assert int(p95[grp]) == int(v[k - 1]), grp
 
+
+
+def test_k3_ragged_sizes_and_value_ranges():
+    """K3 alone (es_scen_p95) on synthetic latency segments: every size class
+    around the 16-byte quads and the CTA width (0 .. 30,001 post-warmup values,
+    base offsets at every alignment), value ranges that take the per-lane coarse
+    bins (< 131 ms), the shared coarse bins (131 ms .. 16.77 s), the overflow
+    radix select (>= 16.77 s), ties and zeros -- against the oracle's nearest-rank
+    P95 (reading Q15) of the post-warmup values."""
+    import torch
+    prof = inputs.Profile(M=1, E=1, bs=np.array([1], np.int32), lat=np.array([[[1000]]], np.uint32),
+                          mask=np.ones((1, 1), np.uint8))
+    W = 5
+    h = es.es_load_profile(prof, [inputs.SchedCfg(tau=50000, b_max=1, warmup=W)])
+    rng = np.random.default_rng(2605)
+    sizes = [0, 3, 5, 6, 7, 8, 9, 10, 12, 13, 36, 38, 261, 262, 1028, 1030, 4104, 12292, 12296, 30006]
+    kinds = ["small", "wide", "ties", "huge", "zeros", "edge"]
+    segs = []
+    for i, n in enumerate(sizes * len(kinds)):
+        kind = kinds[i // len(sizes)]
+        if kind == "small":
+            v = rng.integers(0, 131_000, n)
+        elif kind == "wide":
+            v = rng.integers(0, 16_000_000, n)
+        elif kind == "ties":
+            v = np.full(n, 40_960)
+        elif kind == "huge":
+            v = np.where(rng.random(n) < 0.2, rng.integers(0, 50_000, n), rng.integers(16_777_216, 2**32 - 1, n))
+        elif kind == "zeros":
+            v = np.zeros(n, np.int64)
+        else:  # values on the coarse-bin edges (multiples of 4096 and one below)
+            v = rng.integers(0, 40, n) * 4096 - rng.integers(0, 2, n)
+            v = np.maximum(v, 0)
+        segs.append(np.asarray(v, np.uint32))
+    arr_off = np.zeros(len(segs) + 1, np.uint64)
+    arr_off[1:] = np.cumsum([s.size for s in segs])
+    lat = np.concatenate(segs).astype(np.uint32)
+    dev = "cuda:0"
+    out = {"latency": torch.from_numpy(lat.view(np.int32)).to(dev).view(torch.uint32),
+           "stats": torch.zeros((len(segs), es.ES_NSTAT), dtype=torch.uint64, device=dev),
+           "p95": torch.full((len(segs),), 0xFFFFFFFF, dtype=torch.uint32, device=dev),
+           "dec_cap": 0}
+    d_off = torch.from_numpy(arr_off.view(np.int64)).to(dev).view(torch.uint64)
+    d_arr = torch.zeros(max(1, lat.size), dtype=torch.uint32, device=dev)
+    es.es_scen_p95(h, d_off, d_arr, out)
+    torch.cuda.synchronize()
+    got = np_of(out["p95"])
+    for i, s in enumerate(segs):
+        want = oracle.p95(s[W:]) if s.size > W else 0
+        assert int(got[i]) == want, (i, s.size, kinds[i // len(sizes)])
