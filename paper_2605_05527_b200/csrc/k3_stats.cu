@@ -48,24 +48,8 @@ __device__ uint32_t find_bin(const T *hist, int nbins, uint64_t k, uint64_t *bef
   const int per = (nbins + NT - 1) / NT;
   const int b0 = threadIdx.x * per;
   uint64_t loc = 0;
-  if constexpr (sizeof(T) == 4) {
-    if (nbins == 16 * NT) {  // full 4096-bin histogram (16-byte aligned): 4 x 16-byte loads, 4-way instead of 16-way conflicts
-      const uint4 *h4 = reinterpret_cast<const uint4 *>(hist + b0);
-      uint32_t l32 = 0;
-#pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        const uint4 x = h4[i];
-        l32 += x.x + x.y + x.z + x.w;
-      }
-      loc = l32;  // a CTA histogram of < 2^32 values
-    } else {
-      for (int i = 0; i < per; ++i)
-        if (b0 + i < nbins) loc += (uint64_t)hist[b0 + i];
-    }
-  } else {
-    for (int i = 0; i < per; ++i)
-      if (b0 + i < nbins) loc += (uint64_t)hist[b0 + i];
-  }
+  for (int i = 0; i < per; ++i)
+    if (b0 + i < nbins) loc += (uint64_t)hist[b0 + i];
   // inclusive scan: warp shuffles, then the warp totals
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   uint64_t incl = loc;
@@ -84,6 +68,56 @@ __device__ uint32_t find_bin(const T *hist, int nbins, uint64_t k, uint64_t *bef
     uint64_t run = excl;
     for (int i = 0; i < per && b0 + i < nbins; ++i) {
       const uint64_t h = (uint64_t)hist[b0 + i];
+      if (run + h >= k) {
+        s_bin = (uint32_t)(b0 + i);
+        s_before = run;
+        break;
+      }
+      run += h;
+    }
+  }
+  __syncthreads();
+  *before = s_before;
+  const uint32_t b = s_bin;
+  __syncthreads();
+  return b;
+}
+
+// find_bin for a CTA's own shared-memory histogram (< 2^32 values): 32-bit
+// scan, the warp offsets by one REDUX, the full 4096-bin case read as 16-byte
+// words (4-way instead of 16-way bank conflicts)
+__device__ uint32_t find_bin32(const uint32_t *hist, int nbins, uint32_t k, uint32_t *before) {
+  __shared__ uint32_t s_warp[NW];
+  __shared__ uint32_t s_bin, s_before;
+  const int per = (nbins + NT - 1) / NT;
+  const int b0 = threadIdx.x * per;
+  uint32_t loc = 0;
+  if (nbins == 16 * NT) {
+    const uint4 *h4 = reinterpret_cast<const uint4 *>(hist + b0);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const uint4 x = h4[i];
+      loc += x.x + x.y + x.z + x.w;
+    }
+  } else {
+    for (int i = 0; i < per; ++i)
+      if (b0 + i < nbins) loc += hist[b0 + i];
+  }
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  uint32_t incl = loc;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t v = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += v;
+  }
+  if (lane == 31) s_warp[wid] = incl;
+  __syncthreads();
+  incl += __reduce_add_sync(0xffffffffu, lane < wid ? s_warp[lane] : 0u);
+  const uint32_t excl = incl - loc;
+  if (excl < k && k <= incl) {
+    uint32_t run = excl;
+    for (int i = 0; i < per && b0 + i < nbins; ++i) {
+      const uint32_t h = hist[b0 + i];
       if (run + h >= k) {
         s_bin = (uint32_t)(b0 + i);
         s_before = run;
@@ -239,9 +273,9 @@ __global__ void __launch_bounds__(NT, MINB) k3_stats(StatsArgs a) {
         if (hist[i]) atomicAdd(gh + i, (unsigned long long)hist[i]);
     }
     if (a.p95) {
-      uint64_t kk = (95ull * n + 99ull) / 100ull;  // ceil(0.95 n), 1-based rank
-      uint64_t before;
-      const uint32_t cb = find_bin(hist, (int)top + 1, kk, &before);  // syncs: flush reads done
+      uint32_t kk = (uint32_t)((95ull * n + 99ull) / 100ull);  // ceil(0.95 n), 1-based rank
+      uint32_t before;
+      const uint32_t cb = find_bin32(hist, (int)top + 1, kk, &before);  // syncs: flush reads done
       uint32_t res;
       for (uint32_t i = threadIdx.x; i <= top; i += NT) hist[i] = 0u;
       __syncthreads();
@@ -253,7 +287,7 @@ __global__ void __launch_bounds__(NT, MINB) k3_stats(StatsArgs a) {
           if (d < 4096u) atomicAdd(&hist[d], 1u);
         });
         __syncthreads();
-        const uint32_t fb = find_bin(hist, BINS, kk, &before);
+        const uint32_t fb = find_bin32(hist, BINS, kk, &before);
         res = (cb << 12) | fb;
       } else {  // the rank falls among T >= 16.77 s: radix select from the top bit
         const uint32_t nbits = 32u - __clz(vmax);
@@ -270,7 +304,7 @@ __global__ void __launch_bounds__(NT, MINB) k3_stats(StatsArgs a) {
             if (((uint64_t)v >> prev) == hv) atomicAdd(&hist[(v >> shift) & dmask], 1u);
           }
           __syncthreads();
-          const uint32_t bb = find_bin(hist, (int)nb, kk, &before);
+          const uint32_t bb = find_bin32(hist, (int)nb, kk, &before);
           kk -= before;
           hv = (hv << (prev - shift)) | bb;
           if (shift == 0u) break;
